@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path of arXiv 1707.02018 on B200: grad f = W* R* (R W x - b).
+
+One step = one wl_grad call on BASELINE.json config 5 (4 x 4096^2 fp32, CDF 9/7, 5 levels,
+symmetric BC, 15-tap sigma=3 Gaussian PSF); it runs every hot-path row (W, R, R*, W*).
+Metric (BASELINE.json): "W* and grad f GB/s and % HBM roofline at 4096^2 fp32; gradient
+evals/sec".  value = grad f GB/s = algorithmic bytes of the step (the sum of its operators'
+minimum bytes) / device time.  W* at config 4 (4096^2 db8, 6 levels,
+zero BC) is reported beside it under "wstar_cfg4".
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl wl|reference]
+
+N > 1 (torchrun): every rank runs the full config-5 batch on its own GPU (replicas, weak
+scaling, no data-path collective -- DESIGN.md "Multi-GPU"); time = max over ranks.
+--impl reference times the fp64 CPU oracle (the only other place bench.py runs oracle/).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "W* and ∇f GB/s and % HBM roofline at 4096² fp32; gradient evals/sec"
+FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback if MEASURED_PEAKS.json is absent
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def grad_bytes(B, N, p, es):
+    """Sum of the operators' minimum bytes: W (N+p) + [R u - b] (3N) + R* (2N) + W* (N+p)."""
+    return es * B * ((N + p) + 3 * N + 2 * N + (N + p))
+
+
+def traffic_from_profiles(kernel_key):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    v = d.get(kernel_key)
+    return None if v is None else float(v)
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons while the timed region runs."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x2: "applications_clocks_setting", 0x80: "hw_power_brake_slowdown",
+               0x1: "gpu_idle", 0x100: "sync_boost", 0x200: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self._stop = [], set(), threading.Event()
+        self.max_mhz = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - GPU box only
+            self.err = str(e)
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": len(self.samples)}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_setup():
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v, ws):
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def time_calls(torch, fn, reps, warmup=3):
+    """Average device ms per call on the current stream (events on the launching stream)."""
+    s = torch.cuda.current_stream()
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(reps):
+        fn()
+    e1.record(s)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+# ------------------------------------------------------------------- oracle arm
+def cpu_oracle_grad_step(c, plan_p_valid, x, b):
+    from oracle import oracle as O
+    t = time.perf_counter()
+    O.grad(x, b, c.levels, c.filt, c.bc)
+    return time.perf_counter() - t
+
+
+def run_reference(args):
+    """--impl reference: the fp64 CPU oracle as it stands, on the host cores (rank 0 only)."""
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    from paper_1707_02018_b200 import inputs
+    c = inputs.CONFIGS[5]
+    lay = O.layout(c.h, c.w, c.levels, c.filt, c.bc)
+    # bounded sample: one of the four images of the config-5 batch per step
+    x, _, bl, nz = inputs.workload(c, lay.p, batch=1)
+    x = inputs.cast(x, c.dtype)
+    b = inputs.cast(O.blur(bl) + nz, c.dtype)
+    for _ in range(args.warmup):
+        cpu_oracle_grad_step(c, lay.p, x, b)
+    t = 0.0
+    for _ in range(args.steps):
+        t += cpu_oracle_grad_step(c, lay.p, x, b)
+    step_s = t / args.steps
+    nbytes = grad_bytes(1, c.h * c.w, lay.p, 4)
+    val = nbytes / step_s / 1e9
+    cores = len(os.sched_getaffinity(0))
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GB/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg5 grad f, 1 of 4 images per step (bounded sample)", "h": c.h, "w": c.w,
+                       "batch": 1, "filter": c.filt, "bc": c.bc, "levels": c.levels},
+            "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cores, "kind": "oracle",
+                             "sample": "1 image of 4096^2 per step (cfg5 has 4)"},
+            "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "grad_evals_per_s": 1.0 / step_s}
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------- GPU arm
+def run_wl(args):
+    import torch
+
+    from paper_1707_02018_b200 import inputs, wl
+
+    ws, rank, local = dist_setup()
+    dev = torch.device("cuda", local)
+    hbm_peak, peak_src = measured_peaks()
+    c = inputs.CONFIGS[5]
+    plan = wl.Plan(c.h, c.w, c.levels, c.filt, c.bc, c.dtype)
+    blur = wl.Blur(c.h, c.w, inputs.BLUR_NTAPS, inputs.BLUR_SIGMA, dtype=c.dtype)
+    B, N, es = c.batch, c.h * c.w, 4
+    # ---- inputs (untimed): x from the seeded generator; b = R(blobs) + noise with the GPU R
+    xp, _, bl, nz = inputs.workload(c, plan.p_valid)
+    x = torch.from_numpy(plan.from_packed(xp.astype(np.float32))).to(dev)
+    blobs_d = torch.from_numpy(bl.astype(np.float32)).to(dev)
+    b = blur.apply(blobs_d) + torch.from_numpy(nz.astype(np.float32)).to(dev)
+    del blobs_d
+    g = torch.empty_like(x)
+    f = torch.zeros(B, dtype=torch.float64, device=dev)
+    wsb = plan._ws(wl.OP_GRAD, B, blur=blur)
+    step = lambda: wl.grad(plan, blur, x, b, out=g, f=f, ws=wsb)  # noqa: E731
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    barrier(ws)
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = wl.launch_count()
+    with ClockSampler(local) as clk:
+        e0.record(s)
+        for _ in range(args.steps):
+            step()
+        e1.record(s)
+        torch.cuda.synchronize()
+    launches = wl.launch_count() - launches0
+    barrier(ws)
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, ws)
+    nbytes = grad_bytes(B, N, plan.p_valid, es)
+    value = ws * nbytes / (ms * 1e-3) / 1e9
+
+    # ---- per-kernel live timing (events on the launching stream) for the roofline object
+    u = torch.empty(B, c.h, c.w, device=dev)
+    sres = torch.empty_like(u)
+    plan.synthesize(x, out=u)
+    reps = max(args.steps, 10)
+    kernels = {}
+    t_res = time_calls(torch, lambda: blur.residual_adjoint(u, b, out=sres), reps)
+    kernels["blur_residual_adjoint"] = {"ms": t_res, "bytes": 3 * N * es * B}
+    p1 = wl.Plan(c.h, c.w, 1, c.filt, c.bc, c.dtype)
+    x1 = torch.empty(B, p1.p_alloc, device=dev)
+    t_a1 = time_calls(torch, lambda: p1.adjoint(u, out=x1), reps)
+    kernels["analysis_level1_Wstar"] = {"ms": t_a1, "bytes": es * B * (N + p1.p_valid)}
+    t_s1 = time_calls(torch, lambda: p1.synthesize(x1, out=u), reps)
+    kernels["synthesis_level1_W"] = {"ms": t_s1, "bytes": es * B * (N + p1.p_valid)}
+    for k in kernels.values():
+        k["GB/s"] = k["bytes"] / (k["ms"] * 1e-3) / 1e9
+        k["frac"] = k["GB/s"] / hbm_peak
+        k["share_of_step"] = k["ms"] / ms
+    dom = max(kernels, key=lambda k: kernels[k]["ms"])
+    dk = kernels[dom]
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": dk["GB/s"], "peak": hbm_peak, "unit": "GB/s",
+                "frac": dk["frac"], "traffic": traffic_from_profiles(dom), "peak_source": peak_src,
+                "bytes_per_launch": dk["bytes"]}
+
+    # ---- W* at config 4 (the metric's other half)
+    c4 = inputs.CONFIGS[4]
+    plan4 = wl.Plan(c4.h, c4.w, c4.levels, c4.filt, c4.bc, c4.dtype)
+    _, y4, _, _ = inputs.workload(c4, plan4.p_valid)
+    y4 = torch.from_numpy(y4.astype(np.float32)).to(dev)
+    x4 = torch.empty(1, plan4.p_alloc, device=dev)
+    ws4 = plan4._ws(wl.OP_ADJOINT, 1)
+    t4 = time_calls(torch, lambda: plan4.adjoint(y4, out=x4, ws=ws4), max(args.steps, 20))
+    b4 = 4 * (c4.h * c4.w + plan4.p_valid)
+    wstar = {"us": t4 * 1e3, "GB/s": b4 / (t4 * 1e-3) / 1e9, "frac": b4 / (t4 * 1e-3) / 1e9 / hbm_peak,
+             "bytes": b4, "config": "cfg4 4096^2 db8 zero 6 levels fp32"}
+    del y4, x4, ws4
+
+    # ---- end to end through the public API with host buffers (pinned), copies inside
+    xh = x.cpu().pin_memory()
+    bh = b.cpu().pin_memory()
+    gh = torch.empty_like(xh).pin_memory()
+    fh = torch.empty(B, dtype=torch.float64).pin_memory()
+    xd2, bd2 = torch.empty_like(x), torch.empty_like(b)
+
+    def e2e_step():
+        xd2.copy_(xh, non_blocking=True)
+        bd2.copy_(bh, non_blocking=True)
+        wl.grad(plan, blur, xd2, bd2, out=g, f=f, ws=wsb)
+        gh.copy_(g, non_blocking=True)
+        fh.copy_(f, non_blocking=True)
+
+    e2e_steps = max(3, min(args.steps, 10))
+    t_e2e = max_over_ranks(time_calls(torch, e2e_step, e2e_steps, warmup=2), ws)
+    e2e = {"value": ws * nbytes / (t_e2e * 1e-3) / 1e9, "unit": "GB/s",
+           "h2d_bytes_per_step": (xh.numel() + bh.numel()) * 4, "d2h_bytes_per_step": gh.numel() * 4 + B * 8,
+           "ms_per_step": t_e2e}
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only, bounded sample)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+        x1h, _, bl1, nz1 = inputs.workload(c, plan.p_valid, batch=1)
+        x1h = inputs.cast(x1h, c.dtype)
+        b1 = inputs.cast(O.blur(bl1) + nz1, c.dtype)
+        reps_cpu = 2
+        t = min(cpu_oracle_grad_step(c, plan.p_valid, x1h, b1) for _ in range(reps_cpu))
+        cpu = {"value": grad_bytes(1, N, plan.p_valid, es) / t / 1e9, "unit": "GB/s",
+               "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+               "sample": f"1 of the 4 cfg5 images (4096^2), best of {reps_cpu}", "s_per_image": t}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": "cfg5: grad f = W* R* (R W x - b), 4 x 4096^2, CDF 9/7, 5 levels, "
+                                       "symmetric BC, 15-tap sigma 3 Gaussian PSF",
+                           "global_batch": B * ws, "h": c.h, "w": c.w, "levels": c.levels, "filter": c.filt,
+                           "bc": c.bc, "parallelism": f"replicas x{ws}",
+                           "l2": "inputs larger than L2 (x + b = 538 MB per step per GPU), no flush",
+                           "bytes_per_step_per_gpu": nbytes},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary(), "grad_evals_per_s": ws / (ms * 1e-3), "images_per_s": ws * B / (ms * 1e-3),
+                "grad_frac_of_hbm_roofline": value / ws / hbm_peak, "wstar_cfg4": wstar, "kernels": kernels}
+        print(json.dumps(line))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="wl", choices=["wl", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_wl(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

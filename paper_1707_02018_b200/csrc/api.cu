@@ -1,0 +1,553 @@
+// C ABI of libwl (include/wl.h): plan construction, validation and the operator drivers.
+// Every operator is a chain of kernel launches on the caller's stream; no host sync.
+//
+//   wl_synthesize  W            coarse -> fine, one synthesis launch per level
+//   wl_adjoint     W*  (Eq. (4))    fine -> coarse, dual filters after (E^dagger)*
+//   wl_analyze     W-dagger          fine -> coarse, analysis filters after E_bc
+//   wl_blur / wl_blur_adjoint   R / R*
+//   wl_blur_residual_adjoint    s = R*(R u - b)   (the middle of P:43-45)
+//   wl_grad        grad f = W* R* (R W x - b)
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "wl_internal.h"
+
+namespace wl {
+std::atomic<int64_t> g_launches{0};
+
+cudaError_t launch_zero(void *ptr, size_t bytes, cudaStream_t s) { return cudaMemsetAsync(ptr, 0, bytes, s); }
+}  // namespace wl
+
+using namespace wl;
+
+namespace {
+
+thread_local std::string t_err = "";
+
+wl_status fail(wl_status st, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  t_err = buf;
+  return st;
+}
+
+wl_status ok() {
+  t_err.clear();
+  return WL_OK;
+}
+
+wl_status cuda_fail(cudaError_t e, const char *what) {
+  return fail(WL_ECUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+size_t align256(size_t v) { return (v + 255) / 256 * 256; }
+
+const char *bc_name(int bc) {
+  switch (bc) {
+    case WL_BC_ZERO: return "zero";
+    case WL_BC_PERIODIC: return "periodic";
+    case WL_BC_SYMMETRIC: return "symmetric";
+    case WL_BC_SYMMETRIC_EDAG: return "symmetric_edag";
+  }
+  return "?";
+}
+
+// pointer checks ------------------------------------------------------------
+wl_status check_dev(const void *p, const char *name, size_t align = 16) {
+  if (!p) return fail(WL_EINVAL, "%s is NULL", name);
+  if (reinterpret_cast<uintptr_t>(p) % align)
+    return fail(WL_EALIGN, "%s = %p is not %zu-byte aligned", name, p, align);
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(WL_EINVAL, "%s = %p is not a CUDA pointer (%s)", name, p, cudaGetErrorString(e));
+  }
+  if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
+    return fail(WL_EINVAL, "%s = %p is not device memory", name, p);
+  return WL_OK;
+}
+
+bool overlap(const void *a, size_t na, const void *b, size_t nb) {
+  auto x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+  return na && nb && x < y + nb && y < x + na;
+}
+
+// workspace carve-up ---------------------------------------------------------
+struct WsLayout {
+  size_t a = 0, b = 0, e = 0, u = 0, s = 0, total = 0;  // byte offsets
+};
+
+WsLayout ws_layout(const wl_plan *p, const wl_blur_plan *bl, wl_op op, int64_t batch) {
+  WsLayout L;
+  size_t es = (size_t)p->es, B = (size_t)batch;
+  size_t off = 0;
+  L.a = off; off = align256(off + B * (size_t)p->ws_a_elems * es);
+  L.b = off; off = align256(off + B * (size_t)p->ws_b_elems * es);
+  L.e = off;
+  if ((op == WL_OP_SYNTHESIZE || op == WL_OP_GRAD) && p->bc == WL_BC_SYMMETRIC_EDAG)
+    off = align256(off + B * (size_t)p->edag_elems * es);
+  L.u = off;
+  L.s = off;
+  if (op == WL_OP_GRAD) {
+    size_t img = B * (size_t)p->h * (size_t)p->w * es;
+    L.u = off; off = align256(off + img);
+    L.s = off; off = align256(off + img);
+  }
+  (void)bl;
+  L.total = off;
+  return L;
+}
+
+// level buffers ---------------------------------------------------------------
+struct Buf {
+  char *ptr;
+  int64_t pitch, bstride;
+};
+
+Buf ll_buf(const wl_plan *p, char *ws, const WsLayout &L, int j) {  // LL_j, 1 <= j < J
+  Buf b;
+  b.ptr = ws + ((j % 2) ? L.a : L.b);
+  b.pitch = p->ll_pitch[j];
+  b.bstride = (j % 2) ? p->ws_a_elems : p->ws_b_elems;
+  return b;
+}
+
+Buf band_buf(const wl_plan *p, const void *x, int idx) {
+  Buf b;
+  b.ptr = (char *)x + (size_t)p->band[idx].offset * (size_t)p->es;
+  b.pitch = p->band[idx].pitch;
+  b.bstride = p->p_alloc;
+  return b;
+}
+
+int lh_index(const wl_plan *p, int j) { return 1 + 3 * (p->J - j); }
+
+// analysis chain (W-dagger when adjoint = false, W* when true) -----------------
+wl_status run_analysis(const wl_plan *p, int64_t batch, const void *img, void *x, char *ws, const WsLayout &L,
+                       bool adjoint, cudaStream_t s) {
+  int ext;
+  if (adjoint)
+    ext = p->bc == WL_BC_PERIODIC ? EXT_PER : (p->bc == WL_BC_SYMMETRIC_EDAG ? EXT_SYM_PADJ : EXT_ZERO);
+  else
+    ext = p->bc == WL_BC_PERIODIC ? EXT_PER : (p->bc == WL_BC_ZERO ? EXT_ZERO : EXT_SYM);
+  for (int j = 1; j <= p->J; j++) {
+    AnalysisArgs a;
+    if (j == 1) {
+      a.in = img;
+      a.in_pitch = p->w;
+      a.in_bstride = p->h * p->w;
+    } else {
+      Buf in = ll_buf(p, ws, L, j - 1);
+      a.in = in.ptr;
+      a.in_pitch = in.pitch;
+      a.in_bstride = in.bstride;
+    }
+    a.n0 = (int)p->n0[j - 1];
+    a.n1 = (int)p->n1[j - 1];
+    Buf ll = (j == p->J) ? band_buf(p, x, 0) : ll_buf(p, ws, L, j);
+    Buf lh = band_buf(p, x, lh_index(p, j)), hl = band_buf(p, x, lh_index(p, j) + 1),
+        hh = band_buf(p, x, lh_index(p, j) + 2);
+    Buf outs[4] = {ll, lh, hl, hh};
+    for (int i = 0; i < 4; i++) {
+      a.out[i] = outs[i].ptr;
+      a.out_pitch[i] = outs[i].pitch;
+      a.out_bstride[i] = outs[i].bstride;
+    }
+    a.m0 = (int)p->n0[j];
+    a.m1 = (int)p->n1[j];
+    a.ext = ext;
+    a.lo = adjoint ? p->fb.d_lo : p->fb.a_lo;
+    a.hi = adjoint ? p->fb.d_hi : p->fb.a_hi;
+    a.L = p->fb.L;
+    a.batch = (int)batch;
+    cudaError_t e = launch_analysis(p->dtype, a, s);
+    if (e != cudaSuccess) return cuda_fail(e, "analysis level launch");
+  }
+  return WL_OK;
+}
+
+// synthesis chain (W) ------------------------------------------------------------
+wl_status run_synthesis(const wl_plan *p, int64_t batch, const void *x, void *img, char *ws, const WsLayout &L,
+                        cudaStream_t s) {
+  const int Lp = p->fb.L - 1;
+  for (int j = p->J; j >= 1; j--) {
+    SynthesisArgs a;
+    Buf ll = (j == p->J) ? band_buf(p, x, 0) : ll_buf(p, ws, L, j);
+    Buf bands[4] = {ll, band_buf(p, x, lh_index(p, j)), band_buf(p, x, lh_index(p, j) + 1),
+                    band_buf(p, x, lh_index(p, j) + 2)};
+    for (int i = 0; i < 4; i++) {
+      a.in[i] = bands[i].ptr;
+      a.in_pitch[i] = bands[i].pitch;
+      a.in_bstride[i] = bands[i].bstride;
+    }
+    a.m0 = (int)p->n0[j];
+    a.m1 = (int)p->n1[j];
+    a.coef_mod = p->bc == WL_BC_PERIODIC;
+    a.lo = p->fb.d_lo;
+    a.hi = p->fb.d_hi;
+    a.L = p->fb.L;
+    a.batch = (int)batch;
+    int64_t n0 = p->n0[j - 1], n1 = p->n1[j - 1];
+    Buf out;
+    if (j == 1) {
+      out.ptr = (char *)img;
+      out.pitch = p->w;
+      out.bstride = p->h * p->w;
+    } else {
+      out = ll_buf(p, ws, L, j - 1);
+    }
+    if (p->bc == WL_BC_SYMMETRIC_EDAG) {
+      // W_P = E_sym^dagger W_zpd: synthesize onto [-L', n+L') per axis, then weighted fold
+      int64_t ep = round_up(n1 + 2 * Lp, 16 / p->es);
+      a.out = ws + L.e;
+      a.out_pitch = ep;
+      a.out_bstride = p->edag_elems;
+      a.N0 = (int)(n0 + 2 * Lp);
+      a.N1 = (int)(n1 + 2 * Lp);
+      a.o0 = -Lp;
+      a.o1 = -Lp;
+      cudaError_t e = launch_synthesis(p->dtype, a, s);
+      if (e != cudaSuccess) return cuda_fail(e, "synthesis level launch");
+      FoldArgs f;
+      f.in = ws + L.e;
+      f.in_pitch = ep;
+      f.in_bstride = p->edag_elems;
+      f.out = out.ptr;
+      f.out_pitch = out.pitch;
+      f.out_bstride = out.bstride;
+      f.n0 = (int)n0;
+      f.n1 = (int)n1;
+      f.Lp = Lp;
+      f.batch = (int)batch;
+      e = launch_fold(p->dtype, f, s);
+      if (e != cudaSuccess) return cuda_fail(e, "fold launch");
+    } else {
+      a.out = out.ptr;
+      a.out_pitch = out.pitch;
+      a.out_bstride = out.bstride;
+      a.N0 = (int)n0;
+      a.N1 = (int)n1;
+      a.o0 = 0;
+      a.o1 = 0;
+      cudaError_t e = launch_synthesis(p->dtype, a, s);
+      if (e != cudaSuccess) return cuda_fail(e, "synthesis level launch");
+    }
+  }
+  return WL_OK;
+}
+
+wl_status check_plan(const wl_plan *p) {
+  if (!p) return fail(WL_EINVAL, "plan is NULL");
+  return WL_OK;
+}
+
+wl_status check_ws(const wl_plan *p, const wl_blur_plan *bl, wl_op op, int64_t batch, void *ws) {
+  size_t need = ws_layout(p, bl, op, batch).total;
+  if (need == 0) return WL_OK;
+  return check_dev(ws, "ws", 256);
+}
+
+wl_status check_io(const void *in, size_t in_bytes, const char *in_name, const void *out, size_t out_bytes,
+                   const char *out_name) {
+  wl_status st = check_dev(in, in_name);
+  if (st) return st;
+  st = check_dev(out, out_name);
+  if (st) return st;
+  if (overlap(in, in_bytes, out, out_bytes)) return fail(WL_EINVAL, "%s and %s overlap", in_name, out_name);
+  return WL_OK;
+}
+
+}  // namespace
+
+// =============================================================== public API
+extern "C" {
+
+const char *wl_last_error(void) { return t_err.c_str(); }
+int64_t wl_launch_count(void) { return g_launches.load(); }
+const char *wl_version(void) { return "wl 0.1 (sm_100a)"; }
+
+wl_status wl_plan_create(wl_plan **out, int64_t h, int64_t w, int levels, wl_filter filter, wl_bc bc,
+                         wl_dtype dtype) {
+  if (!out) return fail(WL_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (h < 1 || w < 1) return fail(WL_ESIZE, "image size h=%lld w=%lld must be >= 1", (long long)h, (long long)w);
+  if (h > (1LL << 30) || w > (1LL << 30)) return fail(WL_ESIZE, "image side > 2^30");
+  if (levels < 1 || levels > WL_MAX_LEVELS)
+    return fail(WL_ESIZE, "levels=%d must be in [1, %d]", levels, WL_MAX_LEVELS);
+  if (bc < WL_BC_ZERO || bc > WL_BC_SYMMETRIC_EDAG) return fail(WL_EINVAL, "unknown bc %d", (int)bc);
+  if (dtype != WL_F32 && dtype != WL_F64) return fail(WL_EINVAL, "unknown dtype %d", (int)dtype);
+  wl_plan *p = new (std::nothrow) wl_plan();
+  if (!p) return fail(WL_ENOMEM, "plan allocation failed");
+  if (!build_filter_bank(filter, p->fb)) {
+    delete p;
+    return fail(WL_EINVAL, "unknown filter %d", (int)filter);
+  }
+  p->h = h; p->w = w; p->J = levels; p->filter = filter; p->bc = bc; p->dtype = dtype;
+  p->es = dtype == WL_F64 ? 8 : 4;
+  const int L = p->fb.L;
+  const int64_t align = 16 / p->es;
+  p->n0[0] = h;
+  p->n1[0] = w;
+  for (int j = 1; j <= levels; j++) {
+    for (int ax = 0; ax < 2; ax++) {
+      int64_t n = ax == 0 ? p->n0[j - 1] : p->n1[j - 1];
+      const char *an = ax == 0 ? "h" : "w";
+      if (bc == WL_BC_PERIODIC && (n % 2)) {
+        delete p;
+        return fail(WL_ESIZE, "level %d cannot be formed: periodic BC needs an even length, axis %s has %lld", j,
+                    an, (long long)n);
+      }
+      if ((bc == WL_BC_SYMMETRIC || bc == WL_BC_SYMMETRIC_EDAG) && n < L - 1) {
+        delete p;
+        return fail(WL_ESIZE, "level %d cannot be formed: symmetric BC needs length >= L-1 = %d, axis %s has %lld",
+                    j, L - 1, an, (long long)n);
+      }
+      int64_t m = bc == WL_BC_PERIODIC ? n / 2 : (n + L - 1) / 2;
+      if (m < 1) {
+        delete p;
+        return fail(WL_ESIZE, "level %d cannot be formed: axis %s length %lld", j, an, (long long)n);
+      }
+      (ax == 0 ? p->n0 : p->n1)[j] = m;
+    }
+  }
+  // subband table: LL_J, then (LH, HL, HH) for j = J..1
+  int64_t off = 0, pv = 0;
+  auto add = [&](int idx, int64_t rows, int64_t cols) {
+    p->band[idx].offset = off;
+    p->band[idx].rows = rows;
+    p->band[idx].cols = cols;
+    p->band[idx].pitch = round_up(cols, align);
+    off += rows * p->band[idx].pitch;
+    pv += rows * cols;
+  };
+  add(0, p->n0[levels], p->n1[levels]);
+  for (int j = levels; j >= 1; j--)
+    for (int k = 0; k < 3; k++) add(1 + 3 * (levels - j) + k, p->n0[j], p->n1[j]);
+  p->p_alloc = off;
+  p->p_valid = pv;
+  // workspace: LL_1..LL_{J-1}, ping-pong by level parity
+  for (int j = 1; j < levels; j++) {
+    p->ll_pitch[j] = round_up(p->n1[j], align);
+    int64_t e = p->n0[j] * p->ll_pitch[j];
+    if (j % 2) p->ws_a_elems = std::max(p->ws_a_elems, e);
+    else p->ws_b_elems = std::max(p->ws_b_elems, e);
+  }
+  if (bc == WL_BC_SYMMETRIC_EDAG)
+    for (int j = 1; j <= levels; j++)
+      p->edag_elems = std::max(p->edag_elems, (p->n0[j - 1] + 2 * (L - 1)) * round_up(p->n1[j - 1] + 2 * (L - 1), align));
+  *out = p;
+  return ok();
+}
+
+void wl_plan_destroy(wl_plan *plan) { delete plan; }
+
+wl_status wl_plan_query(const wl_plan *p, wl_plan_info *info) {
+  if (check_plan(p)) return WL_EINVAL;
+  if (!info) return fail(WL_EINVAL, "info is NULL");
+  memset(info, 0, sizeof *info);
+  info->levels = p->J;
+  info->filter_length = p->fb.L;
+  info->p_valid = p->p_valid;
+  info->p_alloc = p->p_alloc;
+  for (int j = 0; j <= p->J; j++) {
+    info->h[j] = p->n0[j];
+    info->w[j] = p->n1[j];
+  }
+  for (int i = 0; i < 1 + 3 * p->J; i++) info->band[i] = p->band[i];
+  return ok();
+}
+
+wl_status wl_plan_filters(const wl_plan *p, double *a_lo, double *a_hi, double *d_lo, double *d_hi) {
+  if (check_plan(p)) return WL_EINVAL;
+  size_t n = sizeof(double) * (size_t)p->fb.L;
+  if (a_lo) memcpy(a_lo, p->fb.a_lo, n);
+  if (a_hi) memcpy(a_hi, p->fb.a_hi, n);
+  if (d_lo) memcpy(d_lo, p->fb.d_lo, n);
+  if (d_hi) memcpy(d_hi, p->fb.d_hi, n);
+  return ok();
+}
+
+size_t wl_workspace_bytes(const wl_plan *p, const wl_blur_plan *bl, wl_op op, int64_t batch) {
+  if (!p || batch < 0) return 0;
+  return ws_layout(p, bl, op, batch).total;
+}
+
+static wl_status analysis_entry(const wl_plan *p, int64_t batch, const void *img, void *x, void *ws, void *stream,
+                                bool adjoint, const char *name) {
+  if (check_plan(p)) return WL_EINVAL;
+  if (batch < 0) return fail(WL_EINVAL, "%s: batch=%lld < 0", name, (long long)batch);
+  if (batch == 0) return ok();
+  size_t ib = (size_t)batch * p->h * p->w * p->es, xb = (size_t)batch * p->p_alloc * p->es;
+  wl_status st = check_io(img, ib, "img", x, xb, "x");
+  if (st) return st;
+  if ((st = check_ws(p, nullptr, adjoint ? WL_OP_ADJOINT : WL_OP_ANALYZE, batch, ws))) return st;
+  WsLayout L = ws_layout(p, nullptr, adjoint ? WL_OP_ADJOINT : WL_OP_ANALYZE, batch);
+  if (L.total && (overlap(ws, L.total, img, ib) || overlap(ws, L.total, x, xb)))
+    return fail(WL_EINVAL, "%s: ws overlaps img or x", name);
+  st = run_analysis(p, batch, img, x, (char *)ws, L, adjoint, (cudaStream_t)stream);
+  return st ? st : ok();
+}
+
+wl_status wl_adjoint(const wl_plan *p, int64_t batch, const void *img, void *x, void *ws, void *stream) {
+  return analysis_entry(p, batch, img, x, ws, stream, true, "wl_adjoint");
+}
+
+wl_status wl_analyze(const wl_plan *p, int64_t batch, const void *img, void *x, void *ws, void *stream) {
+  return analysis_entry(p, batch, img, x, ws, stream, false, "wl_analyze");
+}
+
+wl_status wl_synthesize(const wl_plan *p, int64_t batch, const void *x, void *img, void *ws, void *stream) {
+  if (check_plan(p)) return WL_EINVAL;
+  if (batch < 0) return fail(WL_EINVAL, "wl_synthesize: batch=%lld < 0", (long long)batch);
+  if (batch == 0) return ok();
+  size_t ib = (size_t)batch * p->h * p->w * p->es, xb = (size_t)batch * p->p_alloc * p->es;
+  wl_status st = check_io(x, xb, "x", img, ib, "img");
+  if (st) return st;
+  if ((st = check_ws(p, nullptr, WL_OP_SYNTHESIZE, batch, ws))) return st;
+  WsLayout L = ws_layout(p, nullptr, WL_OP_SYNTHESIZE, batch);
+  if (L.total && (overlap(ws, L.total, img, ib) || overlap(ws, L.total, x, xb)))
+    return fail(WL_EINVAL, "wl_synthesize: ws overlaps img or x");
+  st = run_synthesis(p, batch, x, img, (char *)ws, L, (cudaStream_t)stream);
+  return st ? st : ok();
+}
+
+// ------------------------------------------------------------------- blur
+wl_status wl_blur_create(wl_blur_plan **out, int64_t h, int64_t w, const double *taps, int ntaps, wl_bc bc,
+                         wl_dtype dtype) {
+  if (!out) return fail(WL_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!taps) return fail(WL_EINVAL, "taps_host is NULL");
+  if (ntaps < 1 || ntaps > kMaxTaps || ntaps % 2 == 0)
+    return fail(WL_EINVAL, "ntaps=%d must be odd and <= %d", ntaps, kMaxTaps);
+  if (bc != WL_BC_SYMMETRIC) return fail(WL_EINVAL, "blur supports bc=symmetric only (got %s)", bc_name(bc));
+  if (dtype != WL_F32 && dtype != WL_F64) return fail(WL_EINVAL, "unknown dtype %d", (int)dtype);
+  int hw = ntaps / 2;
+  if (h < 1 || w < 1 || h < hw || w < hw)
+    return fail(WL_ESIZE, "blur needs h, w >= ntaps/2 = %d (got h=%lld w=%lld)", hw, (long long)h, (long long)w);
+  double mx = 0;
+  for (int i = 0; i < ntaps; i++) {
+    if (!std::isfinite(taps[i])) return fail(WL_EINVAL, "tap %d is not finite", i);
+    mx = std::fmax(mx, std::fabs(taps[i]));
+  }
+  for (int i = 0; i < ntaps; i++)
+    if (std::fabs(taps[i] - taps[ntaps - 1 - i]) > 1e-15 * mx)
+      return fail(WL_EINVAL, "taps must be symmetric (k[t] = k[-t]); tap %d differs from tap %d", i, ntaps - 1 - i);
+  wl_blur_plan *b = new (std::nothrow) wl_blur_plan();
+  if (!b) return fail(WL_ENOMEM, "blur plan allocation failed");
+  b->h = h; b->w = w; b->dtype = dtype; b->es = dtype == WL_F64 ? 8 : 4; b->ntaps = ntaps;
+  for (int i = 0; i < ntaps; i++) b->taps[i] = taps[i];
+  *out = b;
+  return ok();
+}
+
+wl_status wl_blur_create_gaussian(wl_blur_plan **out, int64_t h, int64_t w, int ntaps, double sigma, wl_bc bc,
+                                  wl_dtype dtype) {
+  if (!(sigma > 0) || !std::isfinite(sigma)) return fail(WL_EINVAL, "sigma=%g must be > 0", sigma);
+  if (ntaps < 1 || ntaps > kMaxTaps || ntaps % 2 == 0)
+    return fail(WL_EINVAL, "ntaps=%d must be odd and <= %d", ntaps, kMaxTaps);
+  double k[kMaxTaps], sum = 0;
+  int hw = ntaps / 2;
+  for (int t = -hw; t <= hw; t++) sum += (k[t + hw] = std::exp(-(double)(t * t) / (2.0 * sigma * sigma)));
+  for (int i = 0; i < ntaps; i++) k[i] /= sum;
+  return wl_blur_create(out, h, w, k, ntaps, bc, dtype);
+}
+
+void wl_blur_destroy(wl_blur_plan *b) { delete b; }
+
+wl_status wl_blur_taps(const wl_blur_plan *b, double *taps, int *ntaps) {
+  if (!b) return fail(WL_EINVAL, "blur is NULL");
+  if (ntaps) *ntaps = b->ntaps;
+  if (taps) memcpy(taps, b->taps, sizeof(double) * (size_t)b->ntaps);
+  return ok();
+}
+
+static wl_status blur_entry(const wl_blur_plan *bl, int64_t batch, const void *in, void *out, void *stream,
+                            const char *name) {
+  if (!bl) return fail(WL_EINVAL, "%s: blur plan is NULL", name);
+  if (batch < 0) return fail(WL_EINVAL, "%s: batch=%lld < 0", name, (long long)batch);
+  if (batch == 0) return ok();
+  size_t ib = (size_t)batch * bl->h * bl->w * bl->es;
+  wl_status st = check_io(in, ib, "in", out, ib, "out");
+  if (st) return st;
+  BlurArgs a;
+  a.in = in; a.b = nullptr; a.out = out; a.f = nullptr; a.h = bl->h; a.w = bl->w;
+  a.ntaps = bl->ntaps; a.taps = bl->taps; a.batch = (int)batch;
+  cudaError_t e = launch_blur(bl->dtype, a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, name);
+  return ok();
+}
+
+wl_status wl_blur(const wl_blur_plan *bl, int64_t batch, const void *in, void *out, void *stream) {
+  return blur_entry(bl, batch, in, out, stream, "wl_blur");
+}
+
+wl_status wl_blur_adjoint(const wl_blur_plan *bl, int64_t batch, const void *in, void *out, void *stream) {
+  // R* = E_sym^T o correlation = R for the symmetric PSFs wl_blur_create accepts (pinned by tests)
+  return blur_entry(bl, batch, in, out, stream, "wl_blur_adjoint");
+}
+
+static wl_status residual_core(const wl_blur_plan *bl, int64_t batch, const void *u, const void *b, void *s,
+                               double *f, cudaStream_t stream) {
+  BlurArgs a;
+  a.in = u; a.b = b; a.out = s; a.f = f; a.h = bl->h; a.w = bl->w;
+  a.ntaps = bl->ntaps; a.taps = bl->taps; a.batch = (int)batch;
+  cudaError_t e = launch_blur_residual(bl->dtype, a, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "blur residual launch");
+  return WL_OK;
+}
+
+wl_status wl_blur_residual_adjoint(const wl_blur_plan *bl, int64_t batch, const void *u, const void *b, void *s,
+                                   double *f_dev, void *stream) {
+  if (!bl) return fail(WL_EINVAL, "blur plan is NULL");
+  if (batch < 0) return fail(WL_EINVAL, "batch=%lld < 0", (long long)batch);
+  if (batch == 0) return ok();
+  size_t ib = (size_t)batch * bl->h * bl->w * bl->es;
+  wl_status st = check_io(u, ib, "u", s, ib, "s");
+  if (st) return st;
+  if ((st = check_dev(b, "b"))) return st;
+  if (overlap(b, ib, s, ib)) return fail(WL_EINVAL, "b and s overlap");
+  if (f_dev && (st = check_dev(f_dev, "f_dev", 8))) return st;
+  st = residual_core(bl, batch, u, b, s, f_dev, (cudaStream_t)stream);
+  return st ? st : ok();
+}
+
+wl_status wl_grad(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, const void *x, const void *b, void *g,
+                  double *f_dev, void *ws, void *stream) {
+  if (check_plan(p)) return WL_EINVAL;
+  if (!bl) return fail(WL_EINVAL, "wl_grad: blur plan is NULL");
+  if (bl->h != p->h || bl->w != p->w)
+    return fail(WL_EINVAL, "wl_grad: blur plan is %lldx%lld but wavelet plan is %lldx%lld", (long long)bl->h,
+                (long long)bl->w, (long long)p->h, (long long)p->w);
+  if (bl->dtype != p->dtype) return fail(WL_EDTYPE, "wl_grad: blur and wavelet plans have different dtypes");
+  if (batch < 0) return fail(WL_EINVAL, "wl_grad: batch=%lld < 0", (long long)batch);
+  if (batch == 0) return ok();
+  size_t ib = (size_t)batch * p->h * p->w * p->es, xb = (size_t)batch * p->p_alloc * p->es;
+  wl_status st = check_io(x, xb, "x", g, xb, "g");
+  if (st) return st;
+  if ((st = check_dev(b, "b"))) return st;
+  if (overlap(b, ib, g, xb)) return fail(WL_EINVAL, "wl_grad: b and g overlap");
+  if (f_dev && (st = check_dev(f_dev, "f_dev", 8))) return st;
+  if ((st = check_ws(p, bl, WL_OP_GRAD, batch, ws))) return st;
+  WsLayout L = ws_layout(p, bl, WL_OP_GRAD, batch);
+  if (overlap(ws, L.total, x, xb) || overlap(ws, L.total, g, xb) || overlap(ws, L.total, b, ib))
+    return fail(WL_EINVAL, "wl_grad: ws overlaps an argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  char *w = (char *)ws;
+  if ((st = run_synthesis(p, batch, x, w + L.u, w, L, s))) return st;          // u = W x
+  if ((st = residual_core(bl, batch, w + L.u, b, w + L.s, f_dev, s))) return st;  // s = R*(R u - b)
+  if ((st = run_analysis(p, batch, w + L.s, g, w, L, true, s))) return st;     // g = W* s
+  return ok();
+}
+
+}  // extern "C"

@@ -1,0 +1,100 @@
+// Internal declarations shared by the host plan code and the CUDA kernels of libwl.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+
+#include "../../include/wl.h"
+
+namespace wl {
+
+constexpr int kMaxL = 16;     // longest filter frame (db8)
+constexpr int kMaxTaps = 31;  // longest blur PSF per axis
+
+struct FilterBank {
+  int L = 0;
+  double a_lo[kMaxL] = {}, a_hi[kMaxL] = {}, d_lo[kMaxL] = {}, d_hi[kMaxL] = {};
+};
+bool build_filter_bank(int filter, FilterBank &fb);
+
+// Extension applied before an analysis pass.
+enum Ext : int { EXT_ZERO = 0, EXT_PER = 1, EXT_SYM = 2, EXT_SYM_PADJ = 3 };
+
+extern std::atomic<int64_t> g_launches;
+
+// ------------------------------------------------------------ launch args
+// All strides/pitches in elements.  Subband order in arrays: LL, LH, HL, HH.
+struct AnalysisArgs {
+  const void *in;
+  int64_t in_pitch, in_bstride;
+  int n0, n1;
+  void *out[4];
+  int64_t out_pitch[4], out_bstride[4];
+  int m0, m1;
+  int ext;
+  const double *lo, *hi;
+  int L;
+  int batch;
+};
+
+struct SynthesisArgs {
+  const void *in[4];
+  int64_t in_pitch[4], in_bstride[4];
+  int m0, m1;
+  int coef_mod;  // 1: coefficient index taken mod m (periodisation); 0: zero outside [0, m)
+  void *out;
+  int64_t out_pitch, out_bstride;
+  int N0, N1;  // output extent
+  int o0, o1;  // output index i <-> extended position t = i + o
+  const double *lo, *hi;
+  int L;
+  int batch;
+};
+
+struct FoldArgs {  // y = diag(1/c) E_sym^T U per axis (W of the SYMMETRIC_EDAG variant)
+  const void *in;
+  int64_t in_pitch, in_bstride;  // U over [-Lp, n+Lp) per axis
+  void *out;
+  int64_t out_pitch, out_bstride;
+  int n0, n1, Lp;
+  int batch;
+};
+
+struct BlurArgs {
+  const void *in;
+  const void *b;  // residual mode only
+  void *out;
+  double *f;      // residual mode only (nullable)
+  int64_t h, w;
+  int ntaps;
+  const double *taps;
+  int batch;
+};
+
+cudaError_t launch_analysis(int dtype, const AnalysisArgs &a, cudaStream_t s);
+cudaError_t launch_synthesis(int dtype, const SynthesisArgs &a, cudaStream_t s);
+cudaError_t launch_fold(int dtype, const FoldArgs &a, cudaStream_t s);
+cudaError_t launch_blur(int dtype, const BlurArgs &a, cudaStream_t s);
+cudaError_t launch_blur_residual(int dtype, const BlurArgs &a, cudaStream_t s);
+cudaError_t launch_zero(void *ptr, size_t bytes, cudaStream_t s);
+
+}  // namespace wl
+
+struct wl_plan {
+  int64_t h = 0, w = 0;
+  int J = 0, filter = 0, bc = 0, dtype = 0, es = 4;
+  wl::FilterBank fb;
+  int64_t n0[WL_MAX_LEVELS + 1] = {}, n1[WL_MAX_LEVELS + 1] = {};
+  wl_subband band[1 + 3 * WL_MAX_LEVELS] = {};
+  int64_t p_valid = 0, p_alloc = 0;
+  int64_t ll_pitch[WL_MAX_LEVELS + 1] = {};  // pitch of LL_j in the workspace
+  int64_t ws_a_elems = 0, ws_b_elems = 0;    // per image: ping-pong LL buffers (odd / even j)
+  int64_t edag_elems = 0;                    // per image: extended U for the EDAG fold
+};
+
+struct wl_blur_plan {
+  int64_t h = 0, w = 0;
+  int dtype = 0, es = 4, ntaps = 0;
+  double taps[wl::kMaxTaps] = {};
+};

@@ -1,0 +1,355 @@
+"""Thin Python binding of libwl (include/wl.h) -- argument marshalling only.
+
+Every step of every operator runs in the CUDA kernels of libwl.so; this module only
+checks tensor metadata, allocates outputs / workspace with torch (device memory is
+plumbing) and passes raw pointers plus the current CUDA stream through ctypes.
+There is no CPU fallback: if libwl.so cannot be loaded, or a tensor is not on a CUDA
+device, the call raises.
+
+Names follow the paper: W = synthesize, W* = adjoint, W-dagger = analyze,
+R = blur, R* = blur_adjoint, grad f = W* R* (R W x - b).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_PKG, "libwl.so")
+
+WL_OK, WL_EINVAL, WL_ESIZE, WL_EDTYPE, WL_EALIGN, WL_ENOMEM, WL_ECUDA = range(7)
+FILTERS = {"haar": 1, "db1": 1, "db2": 2, "db4": 4, "db8": 8, "cdf97": 97}
+BCS = {"zero": 0, "periodic": 1, "symmetric": 2, "symmetric_edag": 3}
+OP_SYNTHESIZE, OP_ADJOINT, OP_ANALYZE, OP_GRAD = range(4)
+MAX_LEVELS = 32
+
+
+class WLError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"wl status {status}: {msg}")
+        self.status = status
+
+
+class _Subband(ctypes.Structure):
+    _fields_ = [("offset", ctypes.c_int64), ("rows", ctypes.c_int64), ("cols", ctypes.c_int64),
+                ("pitch", ctypes.c_int64)]
+
+
+class _PlanInfo(ctypes.Structure):
+    _fields_ = [("levels", ctypes.c_int), ("filter_length", ctypes.c_int), ("p_valid", ctypes.c_int64),
+                ("p_alloc", ctypes.c_int64), ("h", ctypes.c_int64 * (MAX_LEVELS + 1)),
+                ("w", ctypes.c_int64 * (MAX_LEVELS + 1)), ("band", _Subband * (1 + 3 * MAX_LEVELS))]
+
+
+EXPORTS = ("wl_plan_create", "wl_plan_destroy", "wl_plan_query", "wl_plan_filters", "wl_workspace_bytes",
+           "wl_synthesize", "wl_adjoint", "wl_analyze", "wl_blur_create", "wl_blur_create_gaussian",
+           "wl_blur_destroy", "wl_blur_taps", "wl_blur", "wl_blur_adjoint", "wl_blur_residual_adjoint",
+           "wl_grad", "wl_last_error", "wl_launch_count", "wl_version")
+
+_lib = None
+
+
+def lib():
+    """Load libwl.so (built in-tree by __graft_entry__.build()); raise if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        if os.path.exists("/usr/local/cuda/bin/nvcc") or os.environ.get("NVCC"):
+            from ._build import build
+            build()
+        else:
+            raise ImportError(f"{_LIB_PATH} is missing; run __graft_entry__.build() (no CPU fallback exists)")
+    L = ctypes.CDLL(_LIB_PATH)
+    vp, i64, ci, cd = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+    dp = ctypes.POINTER(ctypes.c_double)
+    L.wl_plan_create.argtypes = [ctypes.POINTER(vp), i64, i64, ci, ci, ci, ci]
+    L.wl_plan_destroy.argtypes = [vp]
+    L.wl_plan_destroy.restype = None
+    L.wl_plan_query.argtypes = [vp, ctypes.POINTER(_PlanInfo)]
+    L.wl_plan_filters.argtypes = [vp, dp, dp, dp, dp]
+    L.wl_workspace_bytes.argtypes = [vp, vp, ci, i64]
+    L.wl_workspace_bytes.restype = ctypes.c_size_t
+    for fn in ("wl_synthesize", "wl_adjoint", "wl_analyze"):
+        getattr(L, fn).argtypes = [vp, i64, vp, vp, vp, vp]
+    L.wl_blur_create.argtypes = [ctypes.POINTER(vp), i64, i64, dp, ci, ci, ci]
+    L.wl_blur_create_gaussian.argtypes = [ctypes.POINTER(vp), i64, i64, ci, cd, ci, ci]
+    L.wl_blur_destroy.argtypes = [vp]
+    L.wl_blur_destroy.restype = None
+    L.wl_blur_taps.argtypes = [vp, dp, ctypes.POINTER(ci)]
+    L.wl_blur.argtypes = [vp, i64, vp, vp, vp]
+    L.wl_blur_adjoint.argtypes = [vp, i64, vp, vp, vp]
+    L.wl_blur_residual_adjoint.argtypes = [vp, i64, vp, vp, vp, vp, vp]
+    L.wl_grad.argtypes = [vp, vp, i64, vp, vp, vp, vp, vp, vp]
+    L.wl_last_error.restype = ctypes.c_char_p
+    L.wl_launch_count.restype = ctypes.c_int64
+    L.wl_version.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def _check(status):
+    if status != WL_OK:
+        raise WLError(status, lib().wl_last_error().decode())
+
+
+def launch_count() -> int:
+    return int(lib().wl_launch_count())
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dtype_code(dtype):
+    torch = _torch()
+    if dtype in (torch.float32, "float32", "f32", np.float32):
+        return 0
+    if dtype in (torch.float64, "float64", "f64", np.float64):
+        return 1
+    raise ValueError(f"unsupported dtype {dtype}")
+
+
+def _stream_ptr(stream):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _require(t, name, dtype, shape=None):
+    torch = _torch()
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} has dtype {t.dtype}, plan expects {dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if shape is not None and tuple(t.shape[-len(shape):]) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected [..., {', '.join(map(str, shape))}]")
+
+
+@dataclass(frozen=True)
+class Band:
+    name: str
+    level: int
+    offset: int
+    rows: int
+    cols: int
+    pitch: int
+
+
+class Plan:
+    """Multi-level 2-D wavelet plan: W, W*, W-dagger on [h, w] images (wl_plan_create)."""
+
+    def __init__(self, h, w, levels, filt="cdf97", bc="symmetric", dtype="float32"):
+        L = lib()
+        self.h, self.w, self.levels = int(h), int(w), int(levels)
+        self.filter, self.bc = filt, bc
+        self._dcode = _dtype_code(dtype)
+        self._h = ctypes.c_void_p()
+        _check(L.wl_plan_create(ctypes.byref(self._h), self.h, self.w, self.levels, FILTERS[filt], BCS[bc],
+                                self._dcode))
+        info = _PlanInfo()
+        _check(L.wl_plan_query(self._h, ctypes.byref(info)))
+        self.L = info.filter_length
+        self.p_valid = int(info.p_valid)
+        self.p_alloc = int(info.p_alloc)
+        self.chain_h = [int(info.h[j]) for j in range(self.levels + 1)]
+        self.chain_w = [int(info.w[j]) for j in range(self.levels + 1)]
+        bands = [Band("LL", self.levels, *(int(v) for v in (info.band[0].offset, info.band[0].rows,
+                                                            info.band[0].cols, info.band[0].pitch)))]
+        i = 1
+        for j in range(self.levels, 0, -1):
+            for nm in ("LH", "HL", "HH"):
+                b = info.band[i]
+                bands.append(Band(nm, j, int(b.offset), int(b.rows), int(b.cols), int(b.pitch)))
+                i += 1
+        self.bands = bands
+
+    @property
+    def torch_dtype(self):
+        torch = _torch()
+        return torch.float64 if self._dcode == 1 else torch.float32
+
+    def filters(self):
+        """fp64 (a_lo, a_hi, d_lo, d_hi) as built by the library (host copies)."""
+        arrs = [np.zeros(self.L) for _ in range(4)]
+        ptrs = [a.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) for a in arrs]
+        _check(lib().wl_plan_filters(self._h, *ptrs))
+        return tuple(arrs)
+
+    def workspace_bytes(self, op, batch, blur=None):
+        return int(lib().wl_workspace_bytes(self._h, blur._h if blur is not None else None, op, int(batch)))
+
+    def _ws(self, op, batch, blur=None, ws=None):
+        n = self.workspace_bytes(op, batch, blur)
+        if ws is not None:
+            if ws.numel() * ws.element_size() < n:
+                raise ValueError(f"workspace too small: need {n} bytes")
+            return ws
+        if n == 0:
+            return None
+        torch = _torch()
+        return torch.empty(n, dtype=torch.uint8, device="cuda")
+
+    def _batch_of(self, t, trailing):
+        return int(np.prod(t.shape[:-trailing])) if t.dim() > trailing else 1
+
+    def synthesize(self, x, out=None, ws=None, stream=None):
+        """W: x [..., p_alloc] -> image [..., h, w]."""
+        torch = _torch()
+        _require(x, "x", self.torch_dtype, (self.p_alloc,))
+        B = self._batch_of(x, 1)
+        if out is None:
+            out = torch.empty(x.shape[:-1] + (self.h, self.w), dtype=x.dtype, device=x.device)
+        _require(out, "img", self.torch_dtype, (self.h, self.w))
+        ws = self._ws(OP_SYNTHESIZE, B, ws=ws)
+        _check(lib().wl_synthesize(self._h, B, _ptr(x), _ptr(out), _ptr(ws), _stream_ptr(stream)))
+        return out
+
+    def _analysis(self, fn, op, img, out, ws, stream):
+        torch = _torch()
+        _require(img, "img", self.torch_dtype, (self.h, self.w))
+        B = self._batch_of(img, 2)
+        if out is None:
+            out = torch.empty(img.shape[:-2] + (self.p_alloc,), dtype=img.dtype, device=img.device)
+        _require(out, "x", self.torch_dtype, (self.p_alloc,))
+        ws = self._ws(op, B, ws=ws)
+        _check(fn(self._h, B, _ptr(img), _ptr(out), _ptr(ws), _stream_ptr(stream)))
+        return out
+
+    def adjoint(self, img, out=None, ws=None, stream=None):
+        """W* (true adjoint of W): image [..., h, w] -> x [..., p_alloc]."""
+        return self._analysis(lib().wl_adjoint, OP_ADJOINT, img, out, ws, stream)
+
+    def analyze(self, img, out=None, ws=None, stream=None):
+        """W-dagger (analysis): image [..., h, w] -> x [..., p_alloc]."""
+        return self._analysis(lib().wl_analyze, OP_ANALYZE, img, out, ws, stream)
+
+    # ---- layout helpers (pure index bookkeeping, no arithmetic) ----
+    def to_packed(self, x):
+        """[..., p_alloc] pitched -> [..., p_valid] packed (LL_J, (LH, HL, HH)_J..1), numpy or torch."""
+        parts = []
+        for b in self.bands:
+            seg = x[..., b.offset:b.offset + b.rows * b.pitch].reshape(x.shape[:-1] + (b.rows, b.pitch))
+            parts.append(seg[..., :b.cols].reshape(x.shape[:-1] + (b.rows * b.cols,)))
+        if isinstance(x, np.ndarray):
+            return np.concatenate(parts, axis=-1)
+        return _torch().cat(parts, dim=-1)
+
+    def from_packed(self, xp):
+        """[..., p_valid] packed -> [..., p_alloc] pitched (padding = 0), numpy or torch."""
+        if isinstance(xp, np.ndarray):
+            out = np.zeros(xp.shape[:-1] + (self.p_alloc,), dtype=xp.dtype)
+        else:
+            out = _torch().zeros(xp.shape[:-1] + (self.p_alloc,), dtype=xp.dtype, device=xp.device)
+        src = 0
+        for b in self.bands:
+            n = b.rows * b.cols
+            dst = out[..., b.offset:b.offset + b.rows * b.pitch].reshape(out.shape[:-1] + (b.rows, b.pitch))
+            dst[..., :b.cols] = xp[..., src:src + n].reshape(xp.shape[:-1] + (b.rows, b.cols))
+            src += n
+        return out
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None) and _lib is not None:
+                _lib.wl_plan_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+class Blur:
+    """Separable PSF blur R (and R*) under half-point symmetric BC (wl_blur_create*)."""
+
+    def __init__(self, h, w, ntaps=15, sigma=3.0, taps=None, dtype="float32"):
+        L = lib()
+        self.h, self.w = int(h), int(w)
+        self._dcode = _dtype_code(dtype)
+        self._h = ctypes.c_void_p()
+        if taps is None:
+            _check(L.wl_blur_create_gaussian(ctypes.byref(self._h), self.h, self.w, int(ntaps), float(sigma),
+                                             BCS["symmetric"], self._dcode))
+        else:
+            t = np.ascontiguousarray(taps, dtype=np.float64)
+            _check(L.wl_blur_create(ctypes.byref(self._h), self.h, self.w,
+                                    t.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), t.size, BCS["symmetric"],
+                                    self._dcode))
+
+    @property
+    def torch_dtype(self):
+        torch = _torch()
+        return torch.float64 if self._dcode == 1 else torch.float32
+
+    def taps(self):
+        n = ctypes.c_int()
+        _check(lib().wl_blur_taps(self._h, None, ctypes.byref(n)))
+        arr = np.zeros(n.value)
+        _check(lib().wl_blur_taps(self._h, arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(n)))
+        return arr
+
+    def _run(self, fn, img, out, stream):
+        torch = _torch()
+        _require(img, "in", self.torch_dtype, (self.h, self.w))
+        B = int(np.prod(img.shape[:-2])) if img.dim() > 2 else 1
+        if out is None:
+            out = torch.empty_like(img)
+        _require(out, "out", self.torch_dtype, (self.h, self.w))
+        _check(fn(self._h, B, _ptr(img), _ptr(out), _stream_ptr(stream)))
+        return out
+
+    def apply(self, img, out=None, stream=None):
+        """R."""
+        return self._run(lib().wl_blur, img, out, stream)
+
+    def adjoint(self, img, out=None, stream=None):
+        """R*."""
+        return self._run(lib().wl_blur_adjoint, img, out, stream)
+
+    def residual_adjoint(self, u, b, out=None, f=None, stream=None):
+        """s = R*(R u - b); f (optional float64 [batch] CUDA tensor) <- 1/2 ||R u - b||^2."""
+        torch = _torch()
+        _require(u, "u", self.torch_dtype, (self.h, self.w))
+        _require(b, "b", self.torch_dtype, (self.h, self.w))
+        B = int(np.prod(u.shape[:-2])) if u.dim() > 2 else 1
+        if out is None:
+            out = torch.empty_like(u)
+        if f is not None:
+            _require(f, "f", torch.float64)
+        _check(lib().wl_blur_residual_adjoint(self._h, B, _ptr(u), _ptr(b), _ptr(out), _ptr(f),
+                                              _stream_ptr(stream)))
+        return out
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None) and _lib is not None:
+                _lib.wl_blur_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def grad(plan: Plan, blur: Blur, x, b, out=None, f=None, ws=None, stream=None):
+    """grad f(x) = W* R* (R W x - b); f (optional float64 [batch]) <- 1/2 ||R W x - b||^2."""
+    torch = _torch()
+    _require(x, "x", plan.torch_dtype, (plan.p_alloc,))
+    _require(b, "b", plan.torch_dtype, (plan.h, plan.w))
+    B = int(np.prod(x.shape[:-1])) if x.dim() > 1 else 1
+    if out is None:
+        out = torch.empty_like(x)
+    if f is not None:
+        _require(f, "f", torch.float64)
+    ws = plan._ws(OP_GRAD, B, blur=blur, ws=ws)
+    _check(lib().wl_grad(plan._h, blur._h, B, _ptr(x), _ptr(b), _ptr(out), _ptr(f), _ptr(ws), _stream_ptr(stream)))
+    return out

@@ -1,0 +1,252 @@
+"""GPU parity: libwl (CUDA, through the C ABI) against the fp64 oracle on identical seeded inputs.
+
+Bars (BASELINE.json north_star): relative L2 error per image <= 1e-12 (fp64) / 2e-6 (fp32),
+normalised by the oracle output norm over valid entries; adjoint identity
+|<W x, y> - <x, W* y>| / (||W x|| ||y||) <= 1e-13 / 1e-5 with the inner products taken in
+fp64 on the host from the GPU outputs.  fp32 cases feed the oracle the fp32-rounded inputs.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from oracle.filters import FILTERS, gaussian_taps
+from paper_1707_02018_b200 import inputs, wl
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"float64": 1e-12, "float32": 2e-6}
+ADJ = {"float64": 1e-13, "float32": 1e-5}
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def to_dev(torch, a, dtype):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device="cuda", dtype=getattr(torch, dtype))
+
+
+def host(t):
+    return t.detach().double().cpu().numpy()
+
+
+def rel(a, b):
+    a = a.reshape(a.shape[0], -1) if a.ndim > 1 else a[None]
+    b = b.reshape(b.shape[0], -1) if b.ndim > 1 else b[None]
+    num = np.linalg.norm(a - b, axis=1)
+    den = np.maximum(np.linalg.norm(b, axis=1), 1e-300)
+    return float(np.max(num / den))
+
+
+def shapes_for(bc, filt):
+    if bc == "periodic":
+        return [(64, 96, 3), (48, 40, 2)]
+    return [(37, 45, 2), (130, 97, 3)]
+
+
+CASES = [(f, bc, dt, shp) for f in FILTERS for bc in O.BCS for dt in ("float64", "float32")
+         for shp in shapes_for(bc, f)]
+
+
+@pytest.mark.parametrize("filt,bc,dtype,shape", CASES)
+def test_operators_match_oracle(torch, filt, bc, dtype, shape):
+    h, w, J = shape
+    B = 2
+    plan = wl.Plan(h, w, J, filt, bc, dtype)
+    rng = np.random.default_rng(hash((filt, bc, dtype, shape)) % 2**32)
+    y = inputs.cast(rng.standard_normal((B, h, w)), dtype)
+    xp = inputs.cast(rng.standard_normal((B, plan.p_valid)), dtype)
+    x = plan.from_packed(xp)
+    yd, xd = to_dev(torch, y, dtype), to_dev(torch, x, dtype)
+    # W*
+    g_adj = host(plan.adjoint(yd))
+    assert rel(plan.to_packed(g_adj), O.adjoint(y, J, filt, bc)) <= TOL[dtype]
+    assert np.all(g_adj[:, np.setdiff1d(np.arange(plan.p_alloc), _valid_idx(plan))] == 0)   # padding = 0
+    # W-dagger
+    g_ana = host(plan.analyze(yd))
+    assert rel(plan.to_packed(g_ana), O.analyze(y, J, filt, bc)) <= TOL[dtype]
+    # W
+    g_syn = host(plan.synthesize(xd))
+    assert rel(g_syn, O.synthesize(xp, h, w, J, filt, bc)) <= TOL[dtype]
+    # adjoint identity on the GPU outputs
+    for b in range(B):
+        lhs = np.vdot(g_syn[b], y[b])
+        rhs = np.vdot(xp[b], plan.to_packed(g_adj[b]))
+        assert abs(lhs - rhs) / (np.linalg.norm(g_syn[b]) * np.linalg.norm(y[b])) <= ADJ[dtype]
+    # perfect reconstruction on the GPU (not for the paper-literal variant, which is interior-only)
+    if bc != "symmetric_edag":
+        rec = host(plan.synthesize(plan.analyze(yd)))
+        assert rel(rec, y) <= 10 * TOL[dtype]
+
+
+def _valid_idx(plan):
+    idx = []
+    for b in plan.bands:
+        r = np.arange(b.rows)[:, None] * b.pitch + np.arange(b.cols)[None, :] + b.offset
+        idx.append(r.ravel())
+    return np.concatenate(idx)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("shape", [(33, 47), (64, 64), (100, 37), (7, 300)])
+def test_blur_matches_oracle(torch, dtype, shape):
+    h, w = shape
+    B = 3
+    blur = wl.Blur(h, w, 15, 3.0, dtype=dtype)
+    rng = np.random.default_rng(11)
+    u = inputs.cast(rng.standard_normal((B, h, w)), dtype)
+    b = inputs.cast(rng.standard_normal((B, h, w)), dtype)
+    ud, bd = to_dev(torch, u, dtype), to_dev(torch, b, dtype)
+    assert rel(host(blur.apply(ud)), O.blur(u)) <= TOL[dtype]
+    assert rel(host(blur.adjoint(ud)), O.blur_adjoint(u)) <= TOL[dtype]
+    f = torch.zeros(B, dtype=torch.float64, device="cuda")
+    s = host(blur.residual_adjoint(ud, bd, f=f))
+    r = O.blur(u) - b
+    assert rel(s, O.blur_adjoint(r)) <= TOL[dtype]
+    fref = 0.5 * np.sum(r.reshape(B, -1) ** 2, axis=1)
+    np.testing.assert_allclose(host(f), fref, rtol=10 * TOL[dtype])
+
+
+@pytest.mark.parametrize("ntaps", [1, 3, 9, 31])
+def test_blur_other_psf_sizes(torch, ntaps):
+    h, w = 45, 38
+    taps = gaussian_taps(ntaps, 2.0)
+    blur = wl.Blur(h, w, taps=taps, dtype="float64")
+    u = np.random.default_rng(ntaps).standard_normal((2, h, w))
+    ud = to_dev(torch, u, "float64")
+    assert rel(host(blur.apply(ud)), O.blur(u, taps)) <= 1e-12
+    s = host(blur.residual_adjoint(ud, ud))
+    assert rel(s, O.blur_adjoint(O.blur(u, taps) - u, taps)) <= 1e-12
+
+
+@pytest.mark.parametrize("filt,bc", [("cdf97", "symmetric"), ("db4", "zero"), ("db2", "periodic"),
+                                     ("haar", "symmetric"), ("cdf97", "symmetric_edag"), ("db8", "symmetric")])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_grad_matches_oracle(torch, filt, bc, dtype):
+    h, w, J = (96, 64, 3) if bc == "periodic" else (83, 70, 3)
+    B = 2
+    plan = wl.Plan(h, w, J, filt, bc, dtype)
+    blur = wl.Blur(h, w, 15, 3.0, dtype=dtype)
+    rng = np.random.default_rng(3)
+    xp = inputs.cast(rng.standard_normal((B, plan.p_valid)), dtype)
+    b = inputs.cast(rng.standard_normal((B, h, w)), dtype)
+    f = torch.zeros(B, dtype=torch.float64, device="cuda")
+    g = host(wl.grad(plan, blur, to_dev(torch, plan.from_packed(xp), dtype), to_dev(torch, b, dtype), f=f))
+    gref, fref = O.grad(xp, b, J, filt, bc)
+    assert rel(plan.to_packed(g), gref) <= TOL[dtype]
+    np.testing.assert_allclose(host(f), fref, rtol=10 * TOL[dtype])
+
+
+# ----------------------------------------------------------------- configs
+def test_cfg1_dense_transpose_on_gpu(torch):
+    """BASELINE.json config 1: W* equals the transpose of W assembled column by column (4096 x 4096)."""
+    c = inputs.CONFIGS[1]
+    plan = wl.Plan(c.h, c.w, c.levels, c.filt, c.bc, c.dtype)
+    assert plan.p_valid == plan.p_alloc == 4096
+    eye = torch.eye(4096, dtype=torch.float64, device="cuda")
+    Wcols = plan.synthesize(plan.from_packed(eye)).reshape(4096, 4096)           # row i = W e_i
+    Wstar_rows = plan.to_packed(plan.adjoint(eye.reshape(4096, 64, 64)))        # row k = W* e_k
+    Wm = host(Wcols).T
+    Ws = host(Wstar_rows).T
+    assert np.abs(Wm.T - Ws).max() < 1e-15
+    # orthogonal + periodic: W* = W-dagger = W^{-1}
+    Wd = host(plan.to_packed(plan.analyze(eye.reshape(4096, 64, 64)))).T
+    assert np.abs(Ws - Wd).max() < 1e-14
+    np.testing.assert_allclose(Ws @ Wm, np.eye(4096), rtol=0, atol=1e-13)
+    x, y, _, _ = inputs.workload(c, plan.p_valid)
+    gx = host(plan.synthesize(to_dev(torch, plan.from_packed(x), c.dtype)))
+    assert rel(gx, O.synthesize(x, c.h, c.w, c.levels, c.filt, c.bc)) <= TOL[c.dtype]
+    gy = host(plan.adjoint(to_dev(torch, y, c.dtype)))
+    assert rel(plan.to_packed(gy), O.adjoint(y, c.levels, c.filt, c.bc)) <= TOL[c.dtype]
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4])
+def test_config_operators_full_size(torch, cfg):
+    c = inputs.CONFIGS[cfg]
+    plan = wl.Plan(c.h, c.w, c.levels, c.filt, c.bc, c.dtype)
+    x, y, _, _ = inputs.workload(c, plan.p_valid)
+    x, y = inputs.cast(x, c.dtype), inputs.cast(y, c.dtype)
+    xd, yd = to_dev(torch, plan.from_packed(x), c.dtype), to_dev(torch, y, c.dtype)
+    gw = host(plan.synthesize(xd))
+    assert rel(gw, O.synthesize(x, c.h, c.w, c.levels, c.filt, c.bc)) <= TOL[c.dtype]
+    gs = host(plan.adjoint(yd))
+    assert rel(plan.to_packed(gs), O.adjoint(y, c.levels, c.filt, c.bc)) <= TOL[c.dtype]
+    if "Wdag" in c.ops:
+        ga = host(plan.analyze(yd))
+        assert rel(plan.to_packed(ga), O.analyze(y, c.levels, c.filt, c.bc)) <= TOL[c.dtype]
+    for b in range(c.batch):
+        d = abs(np.vdot(gw[b], y[b]) - np.vdot(x[b], plan.to_packed(gs[b])))
+        assert d / (np.linalg.norm(gw[b]) * np.linalg.norm(y[b])) <= ADJ[c.dtype]
+
+
+def test_cfg5_grad_full_size(torch):
+    c = inputs.CONFIGS[5]
+    plan = wl.Plan(c.h, c.w, c.levels, c.filt, c.bc, c.dtype)
+    blur = wl.Blur(c.h, c.w, inputs.BLUR_NTAPS, inputs.BLUR_SIGMA, dtype=c.dtype)
+    x, _, bl, nz = inputs.workload(c, plan.p_valid)
+    x = inputs.cast(x, c.dtype)
+    b = inputs.cast(O.blur(bl) + nz, c.dtype)
+    f = torch.zeros(c.batch, dtype=torch.float64, device="cuda")
+    g = host(wl.grad(plan, blur, to_dev(torch, plan.from_packed(x), c.dtype), to_dev(torch, b, c.dtype), f=f))
+    gref, fref = O.grad(x, b, c.levels, c.filt, c.bc)
+    assert rel(plan.to_packed(g), gref) <= TOL[c.dtype]
+    np.testing.assert_allclose(host(f), fref, rtol=1e-5)
+
+
+# -------------------------------------------------------------- edge cases
+def test_edge_cases(torch):
+    plan = wl.Plan(40, 36, 2, "db4", "symmetric", "float32")
+    L = wl.lib()
+    img = torch.randn(40, 36, device="cuda")
+    x = torch.empty(plan.p_alloc, device="cuda")
+    # batch 0 is a no-op
+    assert L.wl_adjoint(plan._h, 0, None, None, None, None) == wl.WL_OK
+    # host pointer rejected
+    himg = np.zeros((40, 36), np.float32)
+    ws = plan._ws(wl.OP_ADJOINT, 1)
+    st = L.wl_adjoint(plan._h, 1, himg.ctypes.data, x.data_ptr(), ws.data_ptr(), None)
+    assert st == wl.WL_EINVAL and b"img" in L.wl_last_error()
+    # aliasing rejected
+    big = torch.empty(plan.p_alloc + 40 * 36, device="cuda")
+    st = L.wl_adjoint(plan._h, 1, big.data_ptr(), big.data_ptr() + 64, ws.data_ptr(), None)
+    assert st == wl.WL_EINVAL and b"overlap" in L.wl_last_error()
+    # misaligned pointer rejected
+    st = L.wl_adjoint(plan._h, 1, img.data_ptr() + 4, x.data_ptr(), ws.data_ptr(), None)
+    assert st == wl.WL_EALIGN
+    # negative batch
+    assert L.wl_adjoint(plan._h, -1, img.data_ptr(), x.data_ptr(), ws.data_ptr(), None) == wl.WL_EINVAL
+    # grad with mismatched plans
+    blur = wl.Blur(40, 40)
+    with pytest.raises(wl.WLError):
+        wl.grad(plan, blur, x, img)
+
+
+@pytest.mark.parametrize("filt,bc,shape", [("haar", "zero", (1, 1, 1)), ("db8", "symmetric", (15, 16, 6)),
+                                           ("haar", "periodic", (2, 64, 1)), ("db2", "zero", (3, 200, 5)),
+                                           ("cdf97", "symmetric", (9, 9, 4)), ("db8", "zero", (1, 5, 3))])
+def test_degenerate_shapes(torch, filt, bc, shape):
+    h, w, J = shape
+    for dtype in ("float64", "float32"):
+        plan = wl.Plan(h, w, J, filt, bc, dtype)
+        rng = np.random.default_rng(0)
+        y = inputs.cast(rng.standard_normal((1, h, w)), dtype)
+        xp = inputs.cast(rng.standard_normal((1, plan.p_valid)), dtype)
+        g = host(plan.adjoint(to_dev(torch, y, dtype)))
+        assert rel(plan.to_packed(g), O.adjoint(y, J, filt, bc)) <= TOL[dtype]
+        s = host(plan.synthesize(to_dev(torch, plan.from_packed(xp), dtype)))
+        assert rel(s, O.synthesize(xp, h, w, J, filt, bc)) <= TOL[dtype]
+        a = host(plan.analyze(to_dev(torch, y, dtype)))
+        assert rel(plan.to_packed(a), O.analyze(y, J, filt, bc)) <= TOL[dtype]
+
+
+def test_native_library_was_used(torch):
+    """The CUDA path ran: libwl counts its own kernel launches."""
+    before = wl.launch_count()
+    plan = wl.Plan(64, 64, 3, "cdf97", "symmetric", "float32")
+    plan.adjoint(torch.randn(64, 64, device="cuda"))
+    torch.cuda.synchronize()
+    assert wl.launch_count() - before == 3
