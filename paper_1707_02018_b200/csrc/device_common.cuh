@@ -1,0 +1,63 @@
+// Small device helpers shared by the libwl kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace wl {
+
+// 16-byte vector type of T
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<float> {
+  using type = float4;
+  static constexpr int n = 4;
+};
+template <>
+struct Vec16<double> {
+  using type = double2;
+  static constexpr int n = 2;
+};
+
+template <typename T>
+__device__ __forceinline__ void vec_split(const typename Vec16<T>::type &v, T *out);
+template <>
+__device__ __forceinline__ void vec_split<float>(const float4 &v, float *o) {
+  o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+}
+template <>
+__device__ __forceinline__ void vec_split<double>(const double2 &v, double *o) {
+  o[0] = v.x; o[1] = v.y;
+}
+template <typename T>
+__device__ __forceinline__ typename Vec16<T>::type vec_make(const T *i);
+template <>
+__device__ __forceinline__ float4 vec_make<float>(const float *i) { return make_float4(i[0], i[1], i[2], i[3]); }
+template <>
+__device__ __forceinline__ double2 vec_make<double>(const double *i) { return make_double2(i[0], i[1]); }
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// cp.async 16 bytes global -> shared (L2 only, no L1 allocation)
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gmem_src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem_dst)), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Smallest pitch (elements) >= n whose size in 4-byte words is 4 mod 8: 8 rows read with
+// 16-byte loads at the same column then hit 8 distinct 4-bank groups (conflict-free).
+template <typename T>
+constexpr int conflict_free_pitch(int n) {
+  int words_per = (int)sizeof(T) / 4;
+  int p = n;
+  while (((p * words_per) % 8) != 4) p++;
+  return p;
+}
+
+constexpr int round_up_c(int v, int a) { return (v + a - 1) / a * a; }
+
+}  // namespace wl
