@@ -20,7 +20,7 @@ LIB = os.path.join(PKG, "libwl.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-I", INCLUDE,
-         "--expt-relaxed-constexpr"]
+         "--expt-relaxed-constexpr", "-diag-suppress", "177"]
 
 
 def _sources():
@@ -36,28 +36,30 @@ def _mtime(p):
     return os.path.getmtime(p) if os.path.exists(p) else -1.0
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, lib: str = LIB, obj: str = OBJ,
+          defines=()) -> str:
+    """Compile every csrc source for sm_100a and link `lib` (defines: extra -D flags for A/B builds)."""
+    os.makedirs(obj, exist_ok=True)
     hdr_t = max([_mtime(h) for h in _headers()] + [_mtime(__file__)])
     objs = []
     changed = force
     for src in _sources():
-        obj = os.path.join(OBJ, os.path.basename(src) + ".o")
-        objs.append(obj)
-        if force or _mtime(obj) < max(_mtime(src), hdr_t):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+        o = os.path.join(obj, os.path.basename(src) + ".o")
+        objs.append(o)
+        if force or _mtime(o) < max(_mtime(src), hdr_t):
+            cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", o]
             if ptxas_v and src.endswith(".cu"):
                 cmd += ["-Xptxas", "-v"]
             if verbose:
                 print(" ".join(cmd), file=sys.stderr)
             subprocess.check_call(cmd)
             changed = True
-    if changed or _mtime(LIB) < max(_mtime(o) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-lcuda"]
+    if changed or _mtime(lib) < max(_mtime(o) for o in objs):
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib, *objs, "-lcuda"]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -18,7 +18,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_PKG, "libwl.so")
+_LIB_PATH = os.environ.get("WL_LIB") or os.path.join(_PKG, "libwl.so")   # WL_LIB: A/B builds (tools)
 
 WL_OK, WL_EINVAL, WL_ESIZE, WL_EDTYPE, WL_EALIGN, WL_ENOMEM, WL_ECUDA = range(7)
 FILTERS = {"haar": 1, "db1": 1, "db2": 2, "db4": 4, "db8": 8, "cdf97": 97}
