@@ -6,33 +6,39 @@
 // yhat = half-point symmetric extension of y:  yhat[-1-i] = y[i], yhat[n+i] = y[n-1-i].
 //
 // Streaming column-strip design (DESIGN.md §6 "k_blur_stream"):
-//   A CTA owns TW output columns of one image and a run of output rows; it walks down
-//   extended rows G at a time.  Per iteration
-//     A  cp.async the next G input rows (TW + 2A columns) into a double buffer;
+//   A CTA owns TW output columns of one image and a band of rows; it walks down the band G
+//   extended rows per iteration:
+//     A  the next G u rows (and, residual, the G b rows the next iteration subtracts) land
+//        in a double buffer: one TMA box each, issued by one thread and completed on an
+//        mbarrier (row blocks touching the image top/bottom are gathered row-reflected with
+//        cp.async instead);
 //     B  horizontal pass from a register window -> h1 history (2h carried rows + G new);
 //     C  vertical pass down a column pair (register window over the h1 history) -> output
-//        rows (R), or r = V H u - b written over the b rows in bbuf (residual; b rows are
-//        cp.async-prefetched one iteration ahead like u);
-//     H2 horizontal pass over the r rows -> h2 history;     (residual only)
-//     D  vertical pass over the h2 history -> s rows, stored. (residual only)
-//   The last 2h rows of each history buffer are copied to its head once per iteration, so
-//   every window is addressed with compile-time offsets.
-//   Vertical halos live in the histories and are never recomputed inside a run; horizontal
-//   halos cost 2*HB/TW extra columns.  Work is scheduled persistently: the flattened
-//   (image, strip, row) space is cut into equal contiguous runs, one per resident CTA.
+//        rows (R), or r = V H u - b written over the b rows (residual);
+//     H2 horizontal pass over the r rows -> h2 history;        (residual only)
+//     D  vertical pass over the h2 history -> s rows, stored.  (residual only)
+//   The last 2h rows of each history are copied to its head once per iteration, so every
+//   window is addressed with compile-time offsets; vertical halos are never recomputed
+//   inside a band.  Runs are ordered (image, band, strip) and handed to persistent CTAs,
+//   so CTAs on neighbouring strips stream the same rows together and the horizontal halo
+//   columns are shared through L2.
 //
 // Boundary handling.  With a symmetric PSF, (k * yhat) is itself symmetric about -1/2 and
 // n-1/2, so the reflected halo of the second blur equals the first blur evaluated at the
 // reflected position: r_ext(q) = (k * u_ext)(q) - b_ext(q) for the infinite symmetric
-// extension, which agrees with the single reflection of R on [-n, 2n) (n >= h).  Every
-// load therefore reads source index refl(p) and the passes are plain convolutions.
+// extension, which agrees with the single reflection of R on [-n, 2n) (n >= h).  Rows are
+// reflected when loaded; columns outside the image (zero-filled by TMA) are never read:
+// the horizontal passes read the mirrored column instead (u and r are both symmetric
+// about the image edges), and outputs outside the image are skipped.
 //
 // FP32 arithmetic uses packed FFMA2 (fma.rn.f32x2): vertical passes pair adjacent
 // columns; horizontal passes split each 2h+1-tap sum into (even, odd) tap pairs over
 // naturally aligned sample pairs and add the two halves at the end.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 
 #include "device_common.cuh"
 #include "wl_internal.h"
@@ -70,6 +76,8 @@ __device__ __forceinline__ P zero2() {
 // Source index of extended position p under the infinite half-point symmetric extension.
 __device__ __forceinline__ int refl_inf(int p, int n) {
   if (p >= 0 && p < n) return p;
+  if (p < 0 && p >= -n) return -1 - p;  // single reflections (the only ones a plan with n >= h needs)
+  if (p >= n && p < 2 * n) return 2 * n - 1 - p;
   const int m = 2 * n;
   p %= m;
   if (p < 0) p += m;
@@ -80,67 +88,72 @@ template <typename T, int HW, bool RESID>
 struct BCfg {
   using P = typename Pair<T>::t;
   static constexpr int VEC = Vec16<T>::n;
-  static constexpr int TW = sizeof(T) == 4 ? 128 : 64;  // output columns per strip
+  // output columns per strip: the residual frame NH1 = TW + 2HB is a multiple of the 16-item warps
+  static constexpr int TW = sizeof(T) == 4 ? (RESID ? 112 : 128) : (RESID ? 48 : 64);
   // extended rows per iteration; G >= 2HW keeps the history move [G, G+2HW) -> [0, 2HW) non-overlapping
   static constexpr int G = (2 * HW > 16) ? 32 : 16;
-  static constexpr int V = 8;                            // outputs per thread, horizontal passes
-  static constexpr int VC = 4;                           // output rows per thread, vertical passes
+  static constexpr int V = 8;                               // outputs per item, horizontal passes
+  static constexpr int VC = 4;                              // output rows per item, vertical passes
   static constexpr int HB = RESID ? round_up_c(HW, 4) : 0;  // r columns beyond the tile per side
-  static constexpr int NH1 = TW + 2 * HB;                // columns of the first horizontal pass
-  static constexpr int A = round_up_c(HB + HW, VEC);     // u columns loaded beyond the tile per side
-  static constexpr int UW = TW + 2 * A;
-  static constexpr int NV = UW / VEC;                    // 16-byte chunks per u row
-  static constexpr int OFF1 = A - HB - HW;               // window offset of pass B
-  static constexpr int OFF2 = HB - HW;                   // window offset of pass H2
+  static constexpr int NH1 = TW + 2 * HB;                   // columns of h1 / r
+  static constexpr int A = round_up_c(HB + HW, VEC);        // u columns loaded beyond the tile per side
+  static constexpr int UW = TW + 2 * A;                     // u box width
+  static constexpr int NV = UW / VEC;                       // 16-byte chunks per u row
+  static constexpr int OFF1 = A - HB - HW;                  // window offset of pass B
+  static constexpr int OFF2 = HB - HW;                      // window offset of pass H2
   static constexpr int NW1 = round_up_c(OFF1 + V + 2 * HW, VEC);
   static constexpr int NW2 = round_up_c(OFF2 + V + 2 * HW, VEC);
-  static constexpr int UP = conflict_free_pitch<T>(UW);
-  static constexpr int R1P = conflict_free_pitch<T>(NH1);
-  static constexpr int R2P = conflict_free_pitch<T>(TW);
-  static constexpr int HR = 2 * HW + G;                  // rows of a history buffer (2HW carried + G new)
+  static constexpr int UP = UW;                             // u rows: dense TMA box
+  static constexpr int BP = NH1;                            // b / r rows: dense TMA box
+  static constexpr int H1P = conflict_free_pitch<T>(NH1);
+  static constexpr int H2P = conflict_free_pitch<T>(TW);
+  static constexpr int HR = 2 * HW + G;                     // rows of a history buffer
   static_assert(2 * HW <= G, "history move must not overlap");
   static_assert(NH1 % V == 0 && TW % V == 0, "segments");
   static_assert(8 * (NH1 / V - 1) + NW1 <= UW, "pass B window overruns the u row");
-  static_assert(!RESID || 8 * (TW / V - 1) + NW2 <= NH1, "pass H2 window overruns rbuf");
-  static constexpr int ITEMS_B = (NH1 / V) * G;
+  static_assert(!RESID || 8 * (TW / V - 1) + NW2 <= NH1, "pass H2 window overruns the r row");
+  static constexpr int SEG1 = NH1 / V, SEG2 = TW / V;
+  static constexpr int ITEMS_B = SEG1 * G;
   static constexpr int ITEMS_C = (RESID ? NH1 / 2 : TW / 2) * (G / VC);
-  static constexpr int ITEMS_H2 = RESID ? (TW / V) * G : 0;
+  static constexpr int ITEMS_H2 = RESID ? SEG2 * G : 0;
   static constexpr int ITEMS_D = RESID ? (TW / 2) * (G / VC) : 0;
   static constexpr int NT = round_up_c(std::max(std::max(ITEMS_B, ITEMS_C), std::max(ITEMS_H2, ITEMS_D)), 32);
-  static constexpr int NVB = RESID ? NH1 / VEC : 0;                  // 16-byte chunks per b row
-  static constexpr int NCHUNK = G * (NV + NVB);                       // chunks loaded per iteration
-  static constexpr int NSLOT = (NCHUNK + NT - 1) / NT;                // chunks per thread per iteration
-  static constexpr int MV1 = 2 * HW * (NH1 / VEC);                   // 16-byte moves of h1 history
-  static constexpr int MV2 = RESID ? 2 * HW * (TW / VEC) : 0;        // 16-byte moves of h2 history
+  static constexpr int NVB = RESID ? NH1 / VEC : 0;         // 16-byte chunks per b row
+  static constexpr int NCHUNK = G * (NV + NVB);             // chunks of a gathered (edge) batch
+  static constexpr int MV1 = 2 * HW * (NH1 / VEC);          // 16-byte moves of h1 history
+  static constexpr int MV2 = RESID ? 2 * HW * (TW / VEC) : 0;  // 16-byte moves of h2 history
   static constexpr int NM1 = (MV1 + NT - 1) / NT, NM2 = (MV2 + NT - 1) / NT;
-  static constexpr size_t smem_bytes() {
-    return sizeof(T) * (2 * (size_t)G * UP + (size_t)HR * R1P + (RESID ? 2 * (size_t)G * R1P + (size_t)HR * R2P : 0));
-  }
+  static constexpr int HA = RESID ? 2 * HW : HW;            // first loaded row = r0 - HA
+  // byte offsets of the shared-memory carve-up (TMA destinations first, 128-byte aligned)
+  static constexpr size_t OFF_U = 0;
+  static constexpr size_t OFF_B = OFF_U + round_up_c(2 * G * UP * (int)sizeof(T), 128);
+  static constexpr size_t OFF_H1 = OFF_B + (RESID ? round_up_c(2 * G * BP * (int)sizeof(T), 128) : 0);
+  static constexpr size_t OFF_H2 = OFF_H1 + round_up_c(HR * H1P * (int)sizeof(T), 16);
+  static constexpr size_t OFF_BAR = OFF_H2 + (RESID ? round_up_c(HR * H2P * (int)sizeof(T), 16) : 0);
+  static constexpr size_t OFF_RED = OFF_BAR + 2 * sizeof(uint64_t);
+  static constexpr size_t smem_bytes() { return OFF_RED + (NT / 32) * sizeof(double); }
 };
 
 template <typename T, int HW>
 struct BlurStreamParams {
   using P = typename Pair<T>::t;
+  CUtensorMap tmap_u;        // u: box (UW columns, G rows, 1 image)        (valid if tma)
+  CUtensorMap tmap_b;        // b: box (NH1 columns, G rows, 1 image)       (residual)
   const T *u;
   const T *b;  // residual only
   T *out;
   double *f;   // residual only (nullable)
-  int h, w, nstrips;
-  long long total_rows, rows_per_cta;
+  int h, w, nstrips, nbands, band_rows, nruns;
   int fast;                  // 16-byte aligned rows: cp.async / vector paths allowed
+  int tma;                   // tensor maps valid
   P cc[2 * HW + 1];          // (c[d], c[d]),  c[d] = k[2h - d]: out[i] = sum_d c[d] yhat[i - h + d]
   P ce[HW + 1], co[HW + 1];  // (c[2m], c[2m+1]) and (c[2m-1], c[2m]) (out-of-range taps = 0)
 };
 
-// Horizontal pass: V outputs out[j] = sum_d c[d] win[j + OFF + d] from a VEC-aligned row window.
+// Horizontal pass over a register window: V outputs out[j] = sum_d c[d] win[j + OFF + d].
 template <typename T, int HW, int V, int OFF, int NW>
-__device__ __forceinline__ void hpass(const T *src, const BlurStreamParams<T, HW> &p, T *outv) {
+__device__ __forceinline__ void hpass_win(const T *win, const BlurStreamParams<T, HW> &p, T *outv) {
   using P = typename Pair<T>::t;
-  using Vt = typename Vec16<T>::type;
-  constexpr int VEC = Vec16<T>::n;
-  T win[NW];
-#pragma unroll
-  for (int i = 0; i < NW / VEC; i++) vec_split<T>(reinterpret_cast<const Vt *>(src)[i], win + i * VEC);
 #pragma unroll
   for (int j = 0; j < V; j++) {
     const int s = j + OFF;
@@ -163,6 +176,28 @@ __device__ __forceinline__ void hpass(const T *src, const BlurStreamParams<T, HW
       }
     }
     outv[j] = acc.x + acc.y;
+  }
+}
+
+// Window of a horizontal item: NW samples starting at frame column `fc` of `srow`.  Away
+// from the image edges this is a run of 16-byte loads; an item whose window crosses an
+// edge reads the mirrored column for every sample outside the image (the frame starts at
+// image column f0 and is fw wide; the mirror of every sample a needed output uses lies
+// inside it).
+template <typename T, int NW>
+__device__ __forceinline__ void load_window(T *win, const T *srow, int fc, bool edge, int f0, int fw, int w) {
+  using Vt = typename Vec16<T>::type;
+  constexpr int VEC = Vec16<T>::n;
+  if (!edge) {
+#pragma unroll
+    for (int i = 0; i < NW / VEC; i++) vec_split<T>(reinterpret_cast<const Vt *>(srow + fc)[i], win + i * VEC);
+  } else {
+#pragma unroll
+    for (int i = 0; i < NW; i++) {
+      const int g = f0 + fc + i;
+      const int src = g < 0 ? -1 - g : (g >= w ? 2 * w - 1 - g : g);
+      win[i] = srow[min(max(src - f0, 0), fw - 1)];
+    }
   }
 }
 
@@ -194,81 +229,107 @@ __device__ __forceinline__ void store_pair(T *row, int col, typename Pair<T>::t 
   }
 }
 
+#ifndef WL_BLUR_MINB
+#define WL_BLUR_MINB 3  // fp32 CTAs per SM the register budget is sized for
+#endif
+
 template <typename T, int HW, bool RESID>
-__global__ void __launch_bounds__(BCfg<T, HW, RESID>::NT, (sizeof(T) == 4 && BCfg<T, HW, RESID>::NT <= 320) ? 3 : 1)
-    k_blur_stream(const BlurStreamParams<T, HW> p) {
+__global__ void __launch_bounds__(BCfg<T, HW, RESID>::NT, (sizeof(T) == 4 && BCfg<T, HW, RESID>::NT <= 256) ? WL_BLUR_MINB : 1)
+    k_blur_stream(const __grid_constant__ BlurStreamParams<T, HW> p) {
   using C = BCfg<T, HW, RESID>;
   using P = typename C::P;
   using Vt = typename Vec16<T>::type;
-  constexpr int G = C::G, VC = C::VC, VEC = C::VEC;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T *ubuf = reinterpret_cast<T *>(smem_raw);  // [2][G][UP]   u rows e .. e+G-1
-  T *h1 = ubuf + 2 * G * C::UP;               // [HR][R1P]    h1 rows e-2HW .. e+G-1
-  T *bbuf = h1 + C::HR * C::R1P;              // [2][G][R1P]  b, then r, rows e-HW .. e-HW+G-1  (residual)
-  T *h2 = bbuf + 2 * G * C::R1P;              // [HR][R2P]    h2 rows e-3HW .. e-HW+G-1     (residual)
-  __shared__ double red[C::NT / 32];
+  constexpr int G = C::G, VC = C::VC, VEC = C::VEC, HA = C::HA;
+  // no static shared memory in this kernel: the dynamic window starts at offset 0 (aligned);
+  // indexing smem_raw directly keeps every access in the shared state space (LDS/STS)
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char *sm = smem_raw;
+  T *ubuf = reinterpret_cast<T *>(sm + C::OFF_U);    // [2][G][UP]   u rows e .. e+G-1
+  T *bbuf = reinterpret_cast<T *>(sm + C::OFF_B);    // [2][G][BP]   b, then r, rows e-HW ..    (residual)
+  T *h1 = reinterpret_cast<T *>(sm + C::OFF_H1);     // [HR][H1P]    h1 rows e-2HW .. e+G-1
+  T *h2 = reinterpret_cast<T *>(sm + C::OFF_H2);     // [HR][H2P]    h2 rows e-3HW .. e-HW+G-1  (residual)
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sm + C::OFF_BAR);  // [2] batch barriers
+  double *red = reinterpret_cast<double *>(sm + C::OFF_RED);
 
   const int tid = threadIdx.x;
-  constexpr int HA = RESID ? 2 * HW : HW;  // first loaded row = r0 - HA
-  long long g = (long long)blockIdx.x * p.rows_per_cta;
-  const long long gend = std::min(p.total_rows, g + p.rows_per_cta);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+  }
+  __syncthreads();
+  unsigned phase = 0;  // parity of the completed phases of bar[0] (bit 0) and bar[1] (bit 1)
 
   // per-thread work items of every stage (fixed for the whole kernel)
-  const bool actB = tid < C::ITEMS_B;
-  const int rowB = tid % G, segB = tid / G;
+  const bool actB0 = tid < C::ITEMS_B;
+  const int segB = tid % C::SEG1, rowB = tid / C::SEG1;
   constexpr int NPC = RESID ? C::NH1 / 2 : C::TW / 2;
-  const bool actC = tid < C::ITEMS_C;
+  const bool actC0 = tid < C::ITEMS_C;
   const int mC = tid % NPC, grpC = tid / NPC;
-  const bool actH2 = RESID && tid < C::ITEMS_H2;
-  const bool actD = RESID && tid < C::ITEMS_D;
+  const bool actH0 = RESID && tid < C::ITEMS_H2;
+  const int segH = tid % C::SEG2, rowH = tid / C::SEG2;
+  const bool actD0 = RESID && tid < C::ITEMS_D;
   const int mD = tid % (C::TW / 2), grpD = tid / (C::TW / 2);
-  // chunks of stage A: slot k = row r, 16-byte chunk v of a u row (v < NV) or of a b row
-  int slot[C::NSLOT];  // (r << 16) | v, or -1
-#pragma unroll
-  for (int k = 0; k < C::NSLOT; k++) {
-    const int idx = tid + k * C::NT;
-    const bool isb = idx >= G * C::NV;
-    const int j = isb ? idx - G * C::NV : idx;
-    const int per = isb ? C::NVB : C::NV;
-    slot[k] = idx < C::NCHUNK ? ((j / per) << 16) | (isb ? C::NV + j % per : j % per) : -1;
-  }
 
-  while (g < gend) {
-    const int unit = (int)(g / p.h);
-    const int r0 = (int)(g - (long long)unit * p.h);
-    const int r1 = (int)std::min<long long>(p.h, r0 + (gend - g));
-    g += r1 - r0;
-    const int img = unit / p.nstrips, strip = unit - img * p.nstrips;
+  for (int run = blockIdx.x; run < p.nruns; run += gridDim.x) {
+    const int strip = run % p.nstrips;
+    const int ib = run / p.nstrips;
+    const int band = ib % p.nbands, img = ib / p.nbands;
+    const int r0 = band * p.band_rows;
+    const int r1 = min(p.h, r0 + p.band_rows);
     const int c0 = strip * C::TW;
     const T *u = p.u + (long long)img * p.h * p.w;
     const T *bimg = RESID ? p.b + (long long)img * p.h * p.w : nullptr;
     T *out = p.out + (long long)img * p.h * p.w;
     const int e_begin = r0 - HA;
-    // output row = loaded row - 2*HA; n_it iterations cover output rows [r0, r1)
+    // output row = loaded row - 2*HA (first valid output r0): n_it iterations cover [r0, r1)
     const int n_it = (r1 - r0 + 2 * HA + G - 1) / G;
-    // per-run column facts
-    const int colC = RESID ? c0 - C::HB + 2 * mC : c0 + 2 * mC;      // frame column of stage C's pair
+
+    // per-run item facts: skip items whose outputs are all outside the image (never read)
+    const int oB = c0 - C::HB + C::V * segB;  // image column of B's first output
+    const bool actB = actB0 && oB < p.w && oB + C::V > 0;
+    const int gB = c0 - C::A + C::V * segB;   // image column of B's window start
+    const bool edgeB = gB < 0 || gB + C::NW1 > p.w;
+    const int colC = RESID ? c0 - C::HB + 2 * mC : c0 + 2 * mC;  // image column of C's pair
+    const bool actC = actC0 && colC < p.w && colC + 2 > 0;
     const bool ovecC = p.fast && colC + 1 < p.w;
-    P fmask;                                                          // f counts each pixel once
+    P fmask;  // f counts each in-image pixel of the tile once
     fmask.x = (colC >= c0 && colC < c0 + C::TW && colC < p.w) ? T(1) : T(0);
     fmask.y = (colC + 1 >= c0 && colC + 1 < c0 + C::TW && colC + 1 < p.w) ? T(1) : T(0);
+    const int oH = c0 + C::V * segH;
+    const bool actH = actH0 && oH < p.w;
+    const int gH = c0 - C::HB + C::V * segH;  // image column of H2's window start
+    const bool edgeH = gH < 0 || gH + C::NW2 > p.w;
     const int colD = c0 + 2 * mD;
+    const bool actD = actD0 && colD < p.w;
     const bool ovecD = p.fast && colD + 1 < p.w;
     double fsum = 0.0;
 
-    // stage A: u rows e0 .. e0+G-1 into ubuf slot `ub`; (residual) b rows e0-HW .. into bbuf slot `ub`
-    auto load_rows = [&](int ub, int e0) {
-#pragma unroll
-      for (int k = 0; k < C::NSLOT; k++) {
-        if (slot[k] < 0) continue;
-        const int sl_r = slot[k] >> 16, sl_v = slot[k] & 0xffff;
-        const bool isb = RESID && sl_v >= C::NV;
-        const int v = isb ? sl_v - C::NV : sl_v;
-        const int sr = refl_inf(e0 + sl_r - (isb ? HW : 0), p.h);
-        const int cg = isb ? c0 - C::HB + v * VEC : c0 - C::A + v * VEC;
-        T *dst = isb ? bbuf + (ub * G + sl_r) * C::R1P + v * VEC
-                     : ubuf + (ub * G + sl_r) * C::UP + v * VEC;
-        const T *row = (isb ? bimg : u) + (long long)sr * p.w;
+    // batch k: u rows e_begin + kG .. and (residual) b rows e_begin + kG - HW .. -> slot k & 1.
+    // Returns whether the batch armed its barrier.
+    auto load_batch = [&](int k) -> bool {
+      const int eu = e_begin + k * G, eb = eu - HW;
+      const bool tma_u = p.tma && eu >= 0 && eu + G <= p.h;
+      const bool tma_b = RESID && p.tma && eb >= 0 && eb + G <= p.h;
+      T *ud = ubuf + (k & 1) * G * C::UP;
+      T *bd = bbuf + (k & 1) * G * C::BP;
+      const unsigned bytes = (tma_u ? G * C::UW * sizeof(T) : 0) + (tma_b ? G * C::NH1 * sizeof(T) : 0);
+      if (tid == 0 && bytes) {
+        fence_proxy_async();
+        mbar_arrive_expect_tx(bar + (k & 1), bytes);
+        if (tma_u) tma_load_3d(ud, &p.tmap_u, bar + (k & 1), c0 - C::A, eu, img);
+        if (tma_b) tma_load_3d(bd, &p.tmap_b, bar + (k & 1), c0 - C::HB, eb, img);
+      }
+      const int lo = tma_u ? G * C::NV : 0;
+      const int hi = (RESID && !tma_b) ? C::NCHUNK : G * C::NV;
+      for (int idx = lo + tid; idx < hi; idx += C::NT) {
+        const bool sb = idx >= G * C::NV;
+        const int j = sb ? idx - G * C::NV : idx;
+        const int per = sb ? (C::NVB > 0 ? C::NVB : 1) : C::NV;
+        const int r = j / per, v = j - r * per;
+        const int sr = refl_inf((sb ? eb : eu) + r, p.h);
+        const int cg = (sb ? c0 - C::HB : c0 - C::A) + v * VEC;
+        T *dst = sb ? bd + r * C::BP + v * VEC : ud + r * C::UP + v * VEC;
+        const T *row = (sb ? bimg : u) + (long long)sr * p.w;
         if (p.fast && cg >= 0 && cg + VEC <= p.w) {
           cp_async16(dst, row + cg);
         } else {
@@ -278,28 +339,31 @@ __global__ void __launch_bounds__(BCfg<T, HW, RESID>::NT, (sizeof(T) == 4 && BCf
           *reinterpret_cast<Vt *>(dst) = vec_make<T>(z);
         }
       }
+      return bytes != 0;
     };
 
-    __syncthreads();  // previous run's smem readers are done
-    load_rows(0, e_begin);
+    __syncthreads();  // the previous run's readers of every buffer are done
+    bool armed = load_batch(0);
     cp_async_commit();
     for (int it = 0; it < n_it; it++) {
       const int e = e_begin + it * G;
       cp_async_wait_all();
-      __syncthreads();  // (1) u rows landed; previous D / moves done
-      if (it + 1 < n_it) {
-        load_rows((it + 1) & 1, e + G);
-        cp_async_commit();
+      if (armed) {
+        mbar_wait(bar + (it & 1), (phase >> (it & 1)) & 1);
+        phase ^= 1u << (it & 1);
       }
+      __syncthreads();  // (1) batch it landed; every stage of it-1 finished
+      armed = (it + 1 < n_it) ? load_batch(it + 1) : false;
+      cp_async_commit();
       if (RESID) {
         // carry the last 2HW h2 rows to the head of the h2 history (D of it-1 has finished)
 #pragma unroll
         for (int k = 0; k < C::NM2; k++) {
           const int idx = tid + k * C::NT;
           if (idx < C::MV2) {
-            const int r = idx / (C::TW / VEC), c = idx % (C::TW / VEC);
-            *reinterpret_cast<Vt *>(h2 + r * C::R2P + c * VEC) =
-                *reinterpret_cast<const Vt *>(h2 + (r + G) * C::R2P + c * VEC);
+            const int r = idx / (C::TW / VEC), c = idx - r * (C::TW / VEC);
+            *reinterpret_cast<Vt *>(h2 + r * C::H2P + c * VEC) =
+                *reinterpret_cast<const Vt *>(h2 + (r + G) * C::H2P + c * VEC);
           }
         }
       } else if (it > 0) {
@@ -308,18 +372,20 @@ __global__ void __launch_bounds__(BCfg<T, HW, RESID>::NT, (sizeof(T) == 4 && BCf
         for (int k = 0; k < C::NM1; k++) {
           const int idx = tid + k * C::NT;
           if (idx < C::MV1) {
-            const int r = idx / (C::NH1 / VEC), c = idx % (C::NH1 / VEC);
-            *reinterpret_cast<Vt *>(h1 + r * C::R1P + c * VEC) =
-                *reinterpret_cast<const Vt *>(h1 + (r + G) * C::R1P + c * VEC);
+            const int r = idx / (C::NH1 / VEC), c = idx - r * (C::NH1 / VEC);
+            *reinterpret_cast<Vt *>(h1 + r * C::H1P + c * VEC) =
+                *reinterpret_cast<const Vt *>(h1 + (r + G) * C::H1P + c * VEC);
           }
         }
         __syncthreads();
       }
       // B: horizontal pass of u rows e .. e+G-1 -> h1 rows 2HW .. 2HW+G-1
       if (actB) {
-        T hv[C::V];
-        hpass<T, HW, C::V, C::OFF1, C::NW1>(ubuf + (it & 1) * G * C::UP + rowB * C::UP + C::V * segB, p, hv);
-        Vt *dst = reinterpret_cast<Vt *>(h1 + (2 * HW + rowB) * C::R1P + C::V * segB);
+        T win[C::NW1], hv[C::V];
+        load_window<T, C::NW1>(win, ubuf + ((it & 1) * G + rowB) * C::UP, C::V * segB, edgeB, c0 - C::A, C::UW,
+                               p.w);
+        hpass_win<T, HW, C::V, C::OFF1, C::NW1>(win, p, hv);
+        Vt *dst = reinterpret_cast<Vt *>(h1 + (2 * HW + rowB) * C::H1P + C::V * segB);
 #pragma unroll
         for (int i = 0; i < C::V / VEC; i++) dst[i] = vec_make<T>(hv + i * VEC);
       }
@@ -328,23 +394,19 @@ __global__ void __launch_bounds__(BCfg<T, HW, RESID>::NT, (sizeof(T) == 4 && BCf
       if (actC) {
         const int xb = e - HW + grpC * VC;
         P acc[VC];
-        vpass<T, HW, VC, C::R1P>(h1 + grpC * VC * C::R1P + 2 * mC, p, acc);
+        vpass<T, HW, VC, C::H1P>(h1 + grpC * VC * C::H1P + 2 * mC, p, acc);
         if (RESID) {
+          // f sums r^2 over the item's valid rows; the tile column mask is applied once
           P fa = zero2<P>();
+          const bool rows_in = xb >= r0 && xb + VC <= r1;
 #pragma unroll
           for (int v = 0; v < VC; v++) {
-            P *rb = reinterpret_cast<P *>(bbuf + ((it & 1) * G + grpC * VC + v) * C::R1P + 2 * mC);
+            P *rb = reinterpret_cast<P *>(bbuf + ((it & 1) * G + grpC * VC + v) * C::BP + 2 * mC);
             const P r = sub2(acc[v], *rb);
             *rb = r;
-            const int x = xb + v;
-            if (x >= r0 && x < r1) {
-              P rm;
-              rm.x = r.x * fmask.x;
-              rm.y = r.y * fmask.y;
-              fa = fma2(rm, r, fa);
-            }
+            if (rows_in || (xb + v >= r0 && xb + v < r1)) fa = fma2(r, r, fa);
           }
-          fsum += (double)fa.x + (double)fa.y;
+          fsum += (double)(fa.x * fmask.x) + (double)(fa.y * fmask.y);
         } else {
 #pragma unroll
           for (int v = 0; v < VC; v++) {
@@ -355,11 +417,13 @@ __global__ void __launch_bounds__(BCfg<T, HW, RESID>::NT, (sizeof(T) == 4 && BCf
       }
       if (RESID) {
         __syncthreads();  // (3) r rows complete; h1 readers done
-        // H2: horizontal pass of r rows -> h2 rows 2HW .. 2HW+G-1
-        if (actH2) {
-          T hv[C::V];
-          hpass<T, HW, C::V, C::OFF2, C::NW2>(bbuf + ((it & 1) * G + rowB) * C::R1P + C::V * segB, p, hv);
-          Vt *dst = reinterpret_cast<Vt *>(h2 + (2 * HW + rowB) * C::R2P + C::V * segB);
+        // H2: horizontal pass of r rows -> h2 rows 2HW .. 2HW+G-1 (rows x = e - HW + row)
+        if (actH) {
+          T win[C::NW2], hv[C::V];
+          load_window<T, C::NW2>(win, bbuf + ((it & 1) * G + rowH) * C::BP, C::V * segH, edgeH, c0 - C::HB, C::NH1,
+                                 p.w);
+          hpass_win<T, HW, C::V, C::OFF2, C::NW2>(win, p, hv);
+          Vt *dst = reinterpret_cast<Vt *>(h2 + (2 * HW + rowH) * C::H2P + C::V * segH);
 #pragma unroll
           for (int i = 0; i < C::V / VEC; i++) dst[i] = vec_make<T>(hv + i * VEC);
         }
@@ -368,9 +432,9 @@ __global__ void __launch_bounds__(BCfg<T, HW, RESID>::NT, (sizeof(T) == 4 && BCf
         for (int k = 0; k < C::NM1; k++) {
           const int idx = tid + k * C::NT;
           if (idx < C::MV1) {
-            const int r = idx / (C::NH1 / VEC), c = idx % (C::NH1 / VEC);
-            *reinterpret_cast<Vt *>(h1 + r * C::R1P + c * VEC) =
-                *reinterpret_cast<const Vt *>(h1 + (r + G) * C::R1P + c * VEC);
+            const int r = idx / (C::NH1 / VEC), c = idx - r * (C::NH1 / VEC);
+            *reinterpret_cast<Vt *>(h1 + r * C::H1P + c * VEC) =
+                *reinterpret_cast<const Vt *>(h1 + (r + G) * C::H1P + c * VEC);
           }
         }
         __syncthreads();  // (4)
@@ -378,7 +442,7 @@ __global__ void __launch_bounds__(BCfg<T, HW, RESID>::NT, (sizeof(T) == 4 && BCf
         const int yb = e - 2 * HW + grpD * VC;
         if (actD && yb + VC > r0 && yb < r1) {
           P acc[VC];
-          vpass<T, HW, VC, C::R2P>(h2 + grpD * VC * C::R2P + 2 * mD, p, acc);
+          vpass<T, HW, VC, C::H2P>(h2 + grpD * VC * C::H2P + 2 * mD, p, acc);
 #pragma unroll
           for (int v = 0; v < VC; v++) {
             const int y = yb + v;
@@ -387,6 +451,7 @@ __global__ void __launch_bounds__(BCfg<T, HW, RESID>::NT, (sizeof(T) == 4 && BCf
         }
       }
     }
+    cp_async_wait_all();
     if (RESID && p.f) {
       for (int o = 16; o > 0; o >>= 1) fsum += __shfl_xor_sync(0xffffffffu, fsum, o);
       if ((tid & 31) == 0) red[tid >> 5] = fsum;
@@ -400,11 +465,42 @@ __global__ void __launch_bounds__(BCfg<T, HW, RESID>::NT, (sizeof(T) == 4 && BCf
   }
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link-time libcuda).
+using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled_fn() {
+  static EncodeTiledFn fn = [] {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+// 3-D map over [batch][h][w] with a box of (box_w columns, rows, 1 image); OOB reads are zero.
+template <typename T>
+bool encode_map(CUtensorMap *m, const void *base, int w, int h, int batch, int box_w, int rows) {
+  EncodeTiledFn enc = encode_tiled_fn();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)batch};
+  cuuint64_t strides[2] = {(cuuint64_t)w * sizeof(T), (cuuint64_t)w * h * sizeof(T)};
+  cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+                   const_cast<void *>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 template <typename T, int HW, bool RESID>
 cudaError_t launch_stream(const BlurArgs &a, cudaStream_t s) {
   using C = BCfg<T, HW, RESID>;
-  using P = typename C::P;
   BlurStreamParams<T, HW> p;
+  memset(&p, 0, sizeof p);
   p.u = static_cast<const T *>(a.in);
   p.b = static_cast<const T *>(a.b);
   p.out = static_cast<T *>(a.out);
@@ -416,6 +512,10 @@ cudaError_t launch_stream(const BlurArgs &a, cudaStream_t s) {
               (reinterpret_cast<uintptr_t>(a.out) % 16 == 0);
   if (RESID) fast = fast && (reinterpret_cast<uintptr_t>(a.b) % 16 == 0);
   p.fast = fast;
+  bool tma = fast && a.h >= C::G;
+  if (tma) tma = encode_map<T>(&p.tmap_u, a.in, p.w, p.h, a.batch, C::UW, C::G);
+  if (tma && RESID) tma = encode_map<T>(&p.tmap_b, a.b, p.w, p.h, a.batch, C::NH1, C::G);
+  p.tma = tma;
   double c[2 * HW + 1];
   for (int d = 0; d <= 2 * HW; d++) c[d] = a.taps[2 * HW - d];
   auto cd = [&](int d) { return (d >= 0 && d <= 2 * HW) ? c[d] : 0.0; };
@@ -429,7 +529,6 @@ cudaError_t launch_stream(const BlurArgs &a, cudaStream_t s) {
     p.co[m].x = T(cd(2 * m - 1));
     p.co[m].y = T(cd(2 * m));
   }
-  (void)sizeof(P);
   const size_t smem = C::smem_bytes();
   auto kern = k_blur_stream<T, HW, RESID>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -439,19 +538,20 @@ cudaError_t launch_stream(const BlurArgs &a, cudaStream_t s) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NT, smem);
   if (e != cudaSuccess) return e;
-  occ = std::max(occ, 1);
-  p.total_rows = (long long)a.batch * p.nstrips * p.h;
-  // one run per resident CTA, but at least 4 iterations of rows per run (halo rows amortised)
-  const long long min_rows = 4LL * C::G;
-  long long grid = std::min<long long>((long long)sms * occ, (p.total_rows + min_rows - 1) / min_rows);
-  grid = std::max<long long>(grid, 1);
-  p.rows_per_cta = (p.total_rows + grid - 1) / grid;
-  grid = (p.total_rows + p.rows_per_cta - 1) / p.rows_per_cta;
+  const long long resident = (long long)sms * std::max(occ, 1);
+  // bands: about one (image, band, strip) run per resident CTA, every band >= 4 iterations
+  const long long per_band = (long long)a.batch * p.nstrips;
+  long long nb = std::max<long long>(1, (resident + per_band / 2) / per_band);
+  nb = std::min<long long>(nb, std::max<long long>(1, a.h / (4 * C::G)));
+  p.band_rows = (int)((a.h + nb - 1) / nb);
+  p.nbands = (int)((a.h + p.band_rows - 1) / p.band_rows);
+  p.nruns = (int)(per_band * p.nbands);
+  const int grid = (int)std::min<long long>(p.nruns, resident);
   if (RESID && a.f) {
     e = cudaMemsetAsync(a.f, 0, sizeof(double) * (size_t)a.batch, s);
     if (e != cudaSuccess) return e;
   }
-  kern<<<(unsigned)grid, C::NT, smem, s>>>(p);
+  kern<<<grid, C::NT, smem, s>>>(p);
   g_launches++;
   return cudaGetLastError();
 }
