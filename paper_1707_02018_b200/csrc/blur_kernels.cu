@@ -38,6 +38,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "device_common.cuh"
@@ -45,33 +46,6 @@
 
 namespace wl {
 namespace {
-
-template <typename T>
-struct Pair;
-template <>
-struct Pair<float> {
-  using t = float2;
-};
-template <>
-struct Pair<double> {
-  using t = double2;
-};
-
-__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
-__device__ __forceinline__ double2 fma2(double2 a, double2 b, double2 c) {
-  return make_double2(fma(a.x, b.x, c.x), fma(a.y, b.y, c.y));
-}
-__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
-__device__ __forceinline__ double2 add2(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 sub2(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-template <typename P>
-__device__ __forceinline__ P zero2() {
-  P z;
-  z.x = 0;
-  z.y = 0;
-  return z;
-}
 
 // Source index of extended position p under the infinite half-point symmetric extension.
 __device__ __forceinline__ int refl_inf(int p, int n) {
@@ -143,7 +117,8 @@ struct BlurStreamParams {
   const T *b;  // residual only
   T *out;
   double *f;   // residual only (nullable)
-  int h, w, nstrips, nbands, band_rows, nruns;
+  int h, w, nstrips;
+  RunMap runs;               // (image, strip) columns x row bands
   int fast;                  // 16-byte aligned rows: cp.async / vector paths allowed
   int tma;                   // tensor maps valid
   P cc[2 * HW + 1];          // (c[d], c[d]),  c[d] = k[2h - d]: out[i] = sum_d c[d] yhat[i - h + d]
@@ -270,12 +245,12 @@ __global__ void __launch_bounds__(BCfg<T, HW, RESID>::NT, (sizeof(T) == 4 && BCf
   const bool actD0 = RESID && tid < C::ITEMS_D;
   const int mD = tid % (C::TW / 2), grpD = tid / (C::TW / 2);
 
-  for (int run = blockIdx.x; run < p.nruns; run += gridDim.x) {
-    const int strip = run % p.nstrips;
-    const int ib = run / p.nstrips;
-    const int band = ib % p.nbands, img = ib / p.nbands;
-    const int r0 = band * p.band_rows;
-    const int r1 = min(p.h, r0 + p.band_rows);
+  const int nruns = p.runs.nruns();
+  for (int run = blockIdx.x; run < nruns; run += gridDim.x) {
+    int col, r0, r1;
+    p.runs.get(run, col, r0, r1);
+    const int img = col / p.nstrips, strip = col - img * p.nstrips;
+    if (r0 >= r1) continue;  // (uniform) empty trailing band
     const int c0 = strip * C::TW;
     const T *u = p.u + (long long)img * p.h * p.w;
     const T *bimg = RESID ? p.b + (long long)img * p.h * p.w : nullptr;
@@ -465,37 +440,6 @@ __global__ void __launch_bounds__(BCfg<T, HW, RESID>::NT, (sizeof(T) == 4 && BCf
   }
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no link-time libcuda).
-using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-EncodeTiledFn encode_tiled_fn() {
-  static EncodeTiledFn fn = [] {
-    void *f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      f = nullptr;
-    return reinterpret_cast<EncodeTiledFn>(f);
-  }();
-  return fn;
-}
-
-// 3-D map over [batch][h][w] with a box of (box_w columns, rows, 1 image); OOB reads are zero.
-template <typename T>
-bool encode_map(CUtensorMap *m, const void *base, int w, int h, int batch, int box_w, int rows) {
-  EncodeTiledFn enc = encode_tiled_fn();
-  if (!enc) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)batch};
-  cuuint64_t strides[2] = {(cuuint64_t)w * sizeof(T), (cuuint64_t)w * h * sizeof(T)};
-  cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)rows, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = enc(m, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
-                   const_cast<void *>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
 template <typename T, int HW, bool RESID>
 cudaError_t launch_stream(const BlurArgs &a, cudaStream_t s) {
   using C = BCfg<T, HW, RESID>;
@@ -512,9 +456,10 @@ cudaError_t launch_stream(const BlurArgs &a, cudaStream_t s) {
               (reinterpret_cast<uintptr_t>(a.out) % 16 == 0);
   if (RESID) fast = fast && (reinterpret_cast<uintptr_t>(a.b) % 16 == 0);
   p.fast = fast;
-  bool tma = fast && a.h >= C::G;
-  if (tma) tma = encode_map<T>(&p.tmap_u, a.in, p.w, p.h, a.batch, C::UW, C::G);
-  if (tma && RESID) tma = encode_map<T>(&p.tmap_b, a.b, p.w, p.h, a.batch, C::NH1, C::G);
+  bool tma = fast && a.h >= C::G && !getenv("WL_NO_TMA");  // WL_NO_TMA: debugging / A-B switch
+  const uint64_t rs = (uint64_t)p.w * sizeof(T), is = rs * (uint64_t)p.h;
+  if (tma) tma = encode_tmap_3d(&p.tmap_u, sizeof(T), a.in, p.w, p.h, a.batch, rs, is, C::UW, C::G);
+  if (tma && RESID) tma = encode_tmap_3d(&p.tmap_b, sizeof(T), a.b, p.w, p.h, a.batch, rs, is, C::NH1, C::G);
   p.tma = tma;
   double c[2 * HW + 1];
   for (int d = 0; d <= 2 * HW; d++) c[d] = a.taps[2 * HW - d];
@@ -531,22 +476,12 @@ cudaError_t launch_stream(const BlurArgs &a, cudaStream_t s) {
   }
   const size_t smem = C::smem_bytes();
   auto kern = k_blur_stream<T, HW, RESID>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  long long resident = 0;
+  cudaError_t e = kernel_resident(reinterpret_cast<const void *>(kern), C::NT, smem, &resident);
   if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148, occ = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NT, smem);
-  if (e != cudaSuccess) return e;
-  const long long resident = (long long)sms * std::max(occ, 1);
-  // bands: about one (image, band, strip) run per resident CTA, every band >= 4 iterations
-  const long long per_band = (long long)a.batch * p.nstrips;
-  long long nb = std::max<long long>(1, (resident + per_band / 2) / per_band);
-  nb = std::min<long long>(nb, std::max<long long>(1, a.h / (4 * C::G)));
-  p.band_rows = (int)((a.h + nb - 1) / nb);
-  p.nbands = (int)((a.h + p.band_rows - 1) / p.band_rows);
-  p.nruns = (int)(per_band * p.nbands);
-  const int grid = (int)std::min<long long>(p.nruns, resident);
+  // one run per resident CTA when the columns allow it; every band >= 4 iterations
+  p.runs = RunMap::make((long long)a.batch * p.nstrips, (int)a.h, resident, 4 * C::G, 1);
+  const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
   if (RESID && a.f) {
     e = cudaMemsetAsync(a.f, 0, sizeof(double) * (size_t)a.batch, s);
     if (e != cudaSuccess) return e;

@@ -60,6 +60,40 @@ constexpr int conflict_free_pitch(int n) {
 
 constexpr int round_up_c(int v, int a) { return (v + a - 1) / a * a; }
 
+// Packed pair arithmetic: float2 maps to FFMA2 / FADD2 (sm_100a), double2 to two FMAs.
+template <typename T>
+struct Pair;
+template <>
+struct Pair<float> {
+  using t = float2;
+};
+template <>
+struct Pair<double> {
+  using t = double2;
+};
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ double2 fma2(double2 a, double2 b, double2 c) {
+  return make_double2(fma(a.x, b.x, c.x), fma(a.y, b.y, c.y));
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ double2 add2(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 sub2(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+template <typename P>
+__device__ __forceinline__ P zero2() {
+  P z;
+  z.x = 0;
+  z.y = 0;
+  return z;
+}
+template <typename P, typename T>
+__device__ __forceinline__ P splat2(T v) {
+  P z;
+  z.x = v;
+  z.y = v;
+  return z;
+}
+
 }  // namespace wl
 
 // ---------------------------------------------------------------- mbarrier + TMA (sm_90+)
@@ -94,5 +128,62 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const void *tmap, uint64_
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
       : "memory");
 }
+
+}  // namespace wl
+
+// ---------------------------------------------------------------- persistent run map
+namespace wl {
+
+// Work decomposition of the streaming kernels: `ncols` columns ((image, strip) pairs, image
+// major) of `span` rows each are cut into bands, one run per band.  The first `extra`
+// columns get nb_lo + 1 bands, the rest nb_lo, so the total number of runs can equal the
+// number of resident CTAs exactly (no tail wave) while neighbouring strips keep the same
+// band boundaries (their halo columns are then streamed through L2 at the same time).
+struct RunMap {
+  int ncols, nb_lo, extra, span, align;
+
+  __host__ __device__ int nruns() const { return extra * (nb_lo + 1) + (ncols - extra) * nb_lo; }
+
+  // run -> (column, first row, end row) with rows in [0, span)
+  __device__ __forceinline__ void get(int run, int &col, int &r0, int &r1) const {
+    int band, nb;
+    const int big = extra * (nb_lo + 1);
+    if (run < big) {
+      col = run / (nb_lo + 1);
+      band = run - col * (nb_lo + 1);
+      nb = nb_lo + 1;
+    } else {
+      const int r = run - big;
+      col = extra + r / nb_lo;
+      band = r - (col - extra) * nb_lo;
+      nb = nb_lo;
+    }
+    int br = (span + nb - 1) / nb;
+    br = (br + align - 1) / align * align;
+    r0 = band * br;
+    r1 = r0 + br < span ? r0 + br : span;
+  }
+
+  // host: split so that nruns() == resident when the columns allow it, bands >= min_rows
+  static RunMap make(long long ncols, int span, long long resident, int min_rows, int align) {
+    RunMap m;
+    m.ncols = (int)ncols;
+    m.span = span;
+    m.align = align > 0 ? align : 1;
+    const int max_nb = span / (min_rows > 0 ? min_rows : 1) > 1 ? span / (min_rows > 0 ? min_rows : 1) : 1;
+    if (ncols >= resident) {
+      m.nb_lo = 1;
+      m.extra = 0;
+    } else {
+      m.nb_lo = (int)(resident / ncols);
+      m.extra = (int)(resident % ncols);
+      if (m.nb_lo >= max_nb) {
+        m.nb_lo = max_nb;
+        m.extra = 0;
+      }
+    }
+    return m;
+  }
+};
 
 }  // namespace wl

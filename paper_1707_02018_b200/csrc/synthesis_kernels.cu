@@ -1,0 +1,356 @@
+// W: one 2-D level of the wavelet reconstruction (sm_100a), streaming column-strip kernel.
+//
+// Per axis the level is the exact transpose of the analysis core out[k] = sum_j f[j] yhat[2k+1-j]
+// (readings R1, R5), written in gather form over extended positions t:
+//     y[t] = sum_{q < H} g[2q + 1 - (t & 1)] * c[floor(t/2) + q],      H = L/2,
+// with g = d_lo for the lowpass and d_hi for the highpass coefficients, c taken as zero outside
+// [0, m) (zero / symmetric BC: W crops) or modulo m (periodisation: W wraps).  Output index
+// i <-> extended position t = i + o (o = 0, or -(L-1) for the SYMMETRIC_EDAG variant, whose
+// weighted fold runs afterwards).
+//
+// A CTA owns TW extended output columns of one image and a band of output rows; it walks
+// down the coefficient rows G at a time:
+//   A   the 4 subband windows (G rows x KCW coefficient columns) land in a double buffer:
+//       one TMA box per subband (zero fill = the crop's zero coefficients), issued by one
+//       thread, completed on an mbarrier; periodic plans gather with cp.async instead;
+//   S1  axis-1 synthesis of each coefficient row: (LL, LH) -> VL row, (HL, HH) -> VH row
+//       (FFMA2 with the tap pair (g[2q+1], g[2q]) against a broadcast coefficient) into a
+//       history of H-1 carried + G new V rows;
+//   S0  axis-0 synthesis: output rows 2s and 2s+1 from V rows s .. s+H-1 (FFMA2 over
+//       adjacent output columns), stored as float2 pairs.
+// Runs are ordered (image, band, strip) and handed to persistent CTAs so neighbouring strips
+// share their coefficient halo through L2.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+
+#include "device_common.cuh"
+#include "wl_internal.h"
+
+namespace wl {
+namespace {
+
+constexpr int H_MAX = kMaxL / 2;
+
+template <typename T, int L>
+struct SCfg {
+  using P = typename Pair<T>::t;
+  static constexpr int VEC = Vec16<T>::n;
+  static constexpr int H = L / 2;
+  static constexpr int TW = sizeof(T) == 4 ? 128 : 64;  // extended output columns per strip (even)
+  static constexpr int G = 16;                           // coefficient rows per iteration
+  static constexpr int SP = 8;                           // output column pairs per S1 item
+  static constexpr int VC = 4;                           // s-values (output row pairs) per S0 item
+  static constexpr int KCW = round_up_c(TW / 2 + H - 1, VEC);  // coefficient columns loaded
+  static constexpr int KCP = KCW;                        // dense TMA box rows
+  static constexpr int NWC = round_up_c(SP + H - 1, VEC);  // S1 window per subband
+  static constexpr int NSEG = TW / (2 * SP);
+  static constexpr int TWP = conflict_free_pitch<T>(TW);
+  static constexpr int HR = H - 1 + G;                   // V history rows
+  static_assert(2 * SP * (NSEG - 1) / 2 + NWC <= KCW, "S1 window overruns the coefficient row");
+  static_assert(G >= H - 1, "history move must not overlap");
+  static constexpr int ITEMS1 = NSEG * G;
+  static constexpr int ITEMS0 = (TW / 2) * (G / VC);
+  static constexpr int NT = round_up_c(std::max(ITEMS1, ITEMS0), 32);
+  static constexpr int NCH = KCW / VEC;                  // 16-byte chunks per coefficient row
+  static constexpr size_t BAND_ELEMS = (size_t)G * KCP;  // one subband window
+  static constexpr size_t OFF_C = 0;                     // [2][4][G][KCP]
+  static constexpr size_t OFF_V = OFF_C + round_up_c(2 * 4 * G * KCP * (int)sizeof(T), 128);
+  static constexpr size_t OFF_BAR = OFF_V + 2 * (size_t)HR * TWP * sizeof(T);  // VL, VH histories
+  static constexpr size_t smem_bytes() { return OFF_BAR + 2 * sizeof(uint64_t); }
+};
+
+template <typename T, int L>
+struct SynStreamParams {
+  using P = typename Pair<T>::t;
+  CUtensorMap tmap[4];       // LL, LH, HL, HH windows: box (KCW, G, 1)   (valid if tma)
+  const T *in[4];
+  long long in_pitch[4], in_bstride[4];
+  T *out;
+  long long out_pitch, out_bstride;
+  int m0, m1, coef_mod, N0, N1, o0, o1;
+  int t00, t01;              // first extended row / column of the output span (even)
+  int nstrips;
+  RunMap runs;               // (image, strip) columns x bands of extended output rows
+  int tma, vec_store;
+  P g1lo[H_MAX], g1hi[H_MAX];  // S1 tap pairs (g[2q+1], g[2q])
+  P e_lo[H_MAX], o_lo[H_MAX];  // S0 broadcast taps (g[2q+1], g[2q+1]) and (g[2q], g[2q])
+  P e_hi[H_MAX], o_hi[H_MAX];
+};
+
+template <typename T, int L>
+__global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 3 : 1)
+    k_synth_stream(const __grid_constant__ SynStreamParams<T, L> p) {
+  using C = SCfg<T, L>;
+  using P = typename C::P;
+  using Vt = typename Vec16<T>::type;
+  constexpr int G = C::G, H = C::H, VEC = C::VEC, VC = C::VC, SP = C::SP;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T *cbuf = reinterpret_cast<T *>(smem_raw + C::OFF_C);  // [2][4][G][KCP] coefficient windows
+  T *vl = reinterpret_cast<T *>(smem_raw + C::OFF_V);    // [HR][TWP] VL history (rows s)
+  T *vh = vl + C::HR * C::TWP;                           // [HR][TWP] VH history
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + C::OFF_BAR);
+
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+  }
+  __syncthreads();
+  unsigned phase = 0;
+  // S1 item: segment fastest; S0 item: column pair fastest
+  const bool act1 = tid < C::ITEMS1;
+  const int seg1 = tid % C::NSEG, row1 = tid / C::NSEG;
+  const bool act0 = tid < C::ITEMS0;
+  const int m0c = tid % (C::TW / 2), grp0 = tid / (C::TW / 2);
+
+  const int nruns = p.runs.nruns();
+  for (int run = blockIdx.x; run < nruns; run += gridDim.x) {
+    int col, b0, b1;
+    p.runs.get(run, col, b0, b1);
+    const int img = col / p.nstrips, strip = col - img * p.nstrips;
+    if (b0 >= b1) continue;  // (uniform) empty trailing band
+    const int tr0 = p.t00 + b0;  // even (bands are even)
+    const int tr1 = p.t00 + b1;
+    const int tc0 = p.t01 + strip * C::TW;                            // even
+    const int kc0 = tc0 / 2;                                          // first coefficient column
+    const int s_first = tr0 / 2, s_last = (tr1 - 1) >> 1;
+    const int n_it = (s_last - s_first + H - 1) / G + 1;
+    T *out = p.out + (long long)img * p.out_bstride;
+    // S0 output column pair (extended t = tc0 + 2 m0c, +1) -> output index
+    const int oc = tc0 + 2 * m0c - p.o1;
+    const bool col_in = oc + 1 >= 0 && oc < p.N1;
+    const bool vec_ok = p.vec_store && oc >= 0 && oc + 1 < p.N1;
+
+    // batch k: coefficient rows s_first + kG .. of the 4 subbands -> cbuf[k & 1]
+    auto load_batch = [&](int k) -> bool {
+      const int kr = s_first + k * G;
+      T *dst0 = cbuf + (k & 1) * 4 * C::BAND_ELEMS;
+      if (p.tma) {
+        if (tid == 0) {
+          fence_proxy_async();
+          mbar_arrive_expect_tx(bar + (k & 1), 4 * C::BAND_ELEMS * sizeof(T));
+#pragma unroll
+          for (int bnd = 0; bnd < 4; bnd++) tma_load_3d(dst0 + bnd * C::BAND_ELEMS, &p.tmap[bnd], bar + (k & 1), kc0, kr, img);
+        }
+        return true;
+      }
+      for (int idx = tid; idx < 4 * G * C::NCH; idx += C::NT) {
+        const int bnd = idx / (G * C::NCH), rem = idx - bnd * G * C::NCH;
+        const int r = rem / C::NCH, v = rem - r * C::NCH;
+        int krr = kr + r;
+        const int cg = kc0 + v * VEC;
+        T *dst = dst0 + bnd * C::BAND_ELEMS + r * C::KCP + v * VEC;
+        bool row_ok = true;
+        if (p.coef_mod) {
+          krr %= p.m0;
+          if (krr < 0) krr += p.m0;
+        } else {
+          row_ok = krr >= 0 && krr < p.m0;
+        }
+        const T *row = p.in[bnd] + (long long)img * p.in_bstride[bnd] + (long long)krr * p.in_pitch[bnd];
+        if (row_ok && cg >= 0 && cg + VEC <= p.m1 && ((cg & (VEC - 1)) == 0)) {
+          cp_async16(dst, row + cg);
+        } else {
+          T z[VEC];
+#pragma unroll
+          for (int i = 0; i < VEC; i++) {
+            int c = cg + i;
+            bool ok = row_ok;
+            if (p.coef_mod) {
+              c %= p.m1;
+              if (c < 0) c += p.m1;
+            } else {
+              ok = ok && c >= 0 && c < p.m1;
+            }
+            z[i] = ok ? row[c] : T(0);
+          }
+          *reinterpret_cast<Vt *>(dst) = vec_make<T>(z);
+        }
+      }
+      return false;
+    };
+
+    __syncthreads();  // previous run's readers are done
+    bool armed = load_batch(0);
+    cp_async_commit();
+    for (int it = 0; it < n_it; it++) {
+      cp_async_wait_all();
+      if (armed) {
+        mbar_wait(bar + (it & 1), (phase >> (it & 1)) & 1);
+        phase ^= 1u << (it & 1);
+      }
+      __syncthreads();  // (1) batch it landed; the history move of it-1 is done
+      armed = (it + 1 < n_it) ? load_batch(it + 1) : false;
+      cp_async_commit();
+      // S1: coefficient row r of the batch -> V rows (history index H-1+r), output pairs SP*seg1 ..
+      if (act1) {
+        const T *cb = cbuf + (it & 1) * 4 * C::BAND_ELEMS + row1 * C::KCP + SP * seg1;
+#pragma unroll 1
+        for (int pr = 0; pr < 2; pr++) {  // pr 0: (LL, LH) -> VL; 1: (HL, HH) -> VH
+          T a[C::NWC], d[C::NWC];
+          const Vt *sa = reinterpret_cast<const Vt *>(cb + (2 * pr) * C::BAND_ELEMS);
+          const Vt *sd = reinterpret_cast<const Vt *>(cb + (2 * pr + 1) * C::BAND_ELEMS);
+#pragma unroll
+          for (int i = 0; i < C::NWC / VEC; i++) {
+            vec_split<T>(sa[i], a + i * VEC);
+            vec_split<T>(sd[i], d + i * VEC);
+          }
+          P ov[SP];
+#pragma unroll
+          for (int j = 0; j < SP; j++) ov[j] = zero2<P>();
+#pragma unroll
+          for (int q = 0; q < H; q++) {  // tap-outer: two tap pairs live at a time
+            const P gl = p.g1lo[q], gh = p.g1hi[q];
+#pragma unroll
+            for (int j = 0; j < SP; j++) {
+              ov[j] = fma2(gl, splat2<P>(a[j + q]), ov[j]);
+              ov[j] = fma2(gh, splat2<P>(d[j + q]), ov[j]);
+            }
+          }
+          T *vrow = (pr == 0 ? vl : vh) + (H - 1 + row1) * C::TWP + 2 * SP * seg1;
+#pragma unroll
+          for (int i = 0; i < 2 * SP / VEC; i++) {
+            T tmp[VEC];
+#pragma unroll
+            for (int u = 0; u < VEC; u += 2) {
+              tmp[u] = ov[(i * VEC + u) / 2].x;
+              tmp[u + 1] = ov[(i * VEC + u) / 2].y;
+            }
+            reinterpret_cast<Vt *>(vrow)[i] = vec_make<T>(tmp);
+          }
+        }
+      }
+      __syncthreads();  // (2)
+      // S0: s = s_first + it*G - (H-1) + grp0*VC + v  (history index grp0*VC + v)
+      if (act0 && col_in) {
+        const int sb = s_first + it * G - (H - 1) + grp0 * VC;
+        P wl[VC + H - 1], wh[VC + H - 1];
+#pragma unroll
+        for (int i = 0; i < VC + H - 1; i++) {
+          wl[i] = *reinterpret_cast<const P *>(vl + (grp0 * VC + i) * C::TWP + 2 * m0c);
+          wh[i] = *reinterpret_cast<const P *>(vh + (grp0 * VC + i) * C::TWP + 2 * m0c);
+        }
+        // tap-outer order: only the 4 broadcast tap pairs of one q are live at a time
+        P e[VC], o[VC];
+#pragma unroll
+        for (int v = 0; v < VC; v++) e[v] = o[v] = zero2<P>();
+#pragma unroll
+        for (int q = 0; q < H; q++) {
+          const P el = p.e_lo[q], ol = p.o_lo[q], eh = p.e_hi[q], oh = p.o_hi[q];
+#pragma unroll
+          for (int v = 0; v < VC; v++) {
+            e[v] = fma2(el, wl[v + q], e[v]);
+            o[v] = fma2(ol, wl[v + q], o[v]);
+            e[v] = fma2(eh, wh[v + q], e[v]);
+            o[v] = fma2(oh, wh[v + q], o[v]);
+          }
+        }
+#pragma unroll
+        for (int v = 0; v < VC; v++) {
+          const int s = sb + v;
+          if (s < s_first || s > s_last) continue;
+#pragma unroll
+          for (int par = 0; par < 2; par++) {
+            const int t = 2 * s + par;
+            const int orow = t - p.o0;
+            if (t < tr0 || t >= tr1 || orow < 0 || orow >= p.N0) continue;
+            const P val = par ? o[v] : e[v];
+            T *op = out + (long long)orow * p.out_pitch + oc;
+            if (vec_ok) {
+              *reinterpret_cast<P *>(op) = val;
+            } else {
+              if (oc >= 0 && oc < p.N1) op[0] = val.x;
+              if (oc + 1 >= 0 && oc + 1 < p.N1) op[1] = val.y;
+            }
+          }
+        }
+      }
+      __syncthreads();  // (3) V history readers done
+      // carry V rows [G, G+H-1) to the head of the history
+      for (int idx = tid; idx < 2 * (H - 1) * (C::TW / VEC); idx += C::NT) {
+        const int half = idx / ((H - 1) * (C::TW / VEC));
+        const int rem = idx - half * (H - 1) * (C::TW / VEC);
+        const int r = rem / (C::TW / VEC), c = rem - r * (C::TW / VEC);
+        T *hb = half ? vh : vl;
+        *reinterpret_cast<Vt *>(hb + r * C::TWP + c * VEC) = *reinterpret_cast<const Vt *>(hb + (r + G) * C::TWP + c * VEC);
+      }
+    }
+    cp_async_wait_all();
+  }
+}
+
+template <typename T, int L>
+cudaError_t launch_synth_stream_t(const SynthesisArgs &a, cudaStream_t s) {
+  using C = SCfg<T, L>;
+  static_assert(C::H <= H_MAX, "H_MAX");
+  SynStreamParams<T, L> p;
+  memset(&p, 0, sizeof p);
+  bool tma = !a.coef_mod && !getenv("WL_NO_TMA");  // WL_NO_TMA: debugging / A-B switch
+  for (int i = 0; i < 4; i++) {
+    p.in[i] = static_cast<const T *>(a.in[i]);
+    p.in_pitch[i] = a.in_pitch[i];
+    p.in_bstride[i] = a.in_bstride[i];
+    if (tma)
+      tma = encode_tmap_3d(&p.tmap[i], sizeof(T), a.in[i], (uint64_t)a.m1, (uint64_t)a.m0, (uint64_t)a.batch,
+                           (uint64_t)a.in_pitch[i] * sizeof(T), (uint64_t)a.in_bstride[i] * sizeof(T), C::KCW, C::G);
+  }
+  p.tma = tma;
+  p.out = static_cast<T *>(a.out);
+  p.out_pitch = a.out_pitch;
+  p.out_bstride = a.out_bstride;
+  p.m0 = a.m0; p.m1 = a.m1; p.coef_mod = a.coef_mod;
+  p.N0 = a.N0; p.N1 = a.N1; p.o0 = a.o0; p.o1 = a.o1;
+  p.t00 = 2 * (a.o0 >> 1);
+  // strips start at a column whose coefficient column kc0 = t01/2 is 16-byte aligned: TMA box
+  // coordinates must address 16-byte aligned global columns (odd EDAG offsets would not)
+  p.t01 = 2 * C::VEC * (int)std::floor((double)a.o1 / (2.0 * C::VEC));
+  p.vec_store = (a.o1 % 2 == 0) && (a.out_pitch % 2 == 0) && (a.out_bstride % 2 == 0) &&
+                (reinterpret_cast<uintptr_t>(a.out) % (2 * sizeof(T)) == 0);
+  for (int q = 0; q < C::H; q++) {
+    p.g1lo[q].x = T(a.lo[2 * q + 1]); p.g1lo[q].y = T(a.lo[2 * q]);
+    p.g1hi[q].x = T(a.hi[2 * q + 1]); p.g1hi[q].y = T(a.hi[2 * q]);
+    p.e_lo[q].x = p.e_lo[q].y = T(a.lo[2 * q + 1]);
+    p.o_lo[q].x = p.o_lo[q].y = T(a.lo[2 * q]);
+    p.e_hi[q].x = p.e_hi[q].y = T(a.hi[2 * q + 1]);
+    p.o_hi[q].x = p.o_hi[q].y = T(a.hi[2 * q]);
+  }
+  const int span0 = a.o0 + a.N0 - p.t00, span1 = a.o1 + a.N1 - p.t01;
+  p.nstrips = (span1 + C::TW - 1) / C::TW;
+  const size_t smem = C::smem_bytes();
+  auto kern = k_synth_stream<T, L>;
+  long long resident = 0;
+  cudaError_t e = kernel_resident(reinterpret_cast<const void *>(kern), C::NT, smem, &resident);
+  if (e != cudaSuccess) return e;
+  // one run per resident CTA when the columns allow it; even bands of >= 4 iterations
+  p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident, 8 * C::G, 2);
+  const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
+  kern<<<grid, C::NT, smem, s>>>(p);
+  g_launches++;
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t dispatch(const SynthesisArgs &a, cudaStream_t s) {
+  switch (a.L) {
+    case 2: return launch_synth_stream_t<T, 2>(a, s);
+    case 4: return launch_synth_stream_t<T, 4>(a, s);
+    case 8: return launch_synth_stream_t<T, 8>(a, s);
+    case 10: return launch_synth_stream_t<T, 10>(a, s);
+    case 16: return launch_synth_stream_t<T, 16>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+cudaError_t launch_synthesis(int dtype, const SynthesisArgs &a, cudaStream_t s) {
+  if (a.batch == 0 || a.N0 == 0 || a.N1 == 0) return cudaSuccess;
+  return dtype == WL_F64 ? dispatch<double>(a, s) : dispatch<float>(a, s);
+}
+
+}  // namespace wl

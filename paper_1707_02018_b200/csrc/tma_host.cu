@@ -1,0 +1,96 @@
+// Host-side TMA descriptor encoding for libwl (cuTensorMapEncodeTiled through the runtime's
+// driver entry point, so the library has no link-time dependency on libcuda).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "wl_internal.h"
+
+namespace wl {
+namespace {
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled_fn() {
+  static EncodeTiledFn fn = [] {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+}  // namespace
+
+bool encode_tmap_3d(void *map, int elem_bytes, const void *base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
+                    uint64_t s2, uint32_t box0, uint32_t box1) {
+  // Encoding costs microseconds of host time per descriptor; operators called repeatedly on
+  // the same buffers (solver loops, benchmarks) reuse the cached descriptor.
+  using Key = std::tuple<int, const void *, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t>;
+  static std::mutex mu;
+  static std::map<Key, CUtensorMap> cache;
+  const Key key(elem_bytes, base, d0, d1, d2, s1, s2, box0, box1);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *reinterpret_cast<CUtensorMap *>(map) = it->second;
+      return true;
+    }
+  }
+  EncodeTiledFn enc = encode_tiled_fn();
+  if (!enc || !base || (reinterpret_cast<uintptr_t>(base) & 15) || (s1 & 15) || (s2 & 15)) return false;
+  if (box0 == 0 || box1 == 0 || box0 > 256 || box1 > 256 || (box0 * (uint32_t)elem_bytes) % 16) return false;
+  cuuint64_t dims[3] = {d0, d1, d2 > 0 ? d2 : 1};
+  cuuint64_t strides[2] = {s1, s2 > 0 ? s2 : s1 * d1};
+  cuuint32_t box[3] = {box0, box1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(reinterpret_cast<CUtensorMap *>(map),
+                   elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+                   const_cast<void *>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  std::lock_guard<std::mutex> g(mu);
+  if (cache.size() > 4096) cache.clear();
+  cache[key] = *reinterpret_cast<CUtensorMap *>(map);
+  return true;
+}
+
+cudaError_t kernel_resident(const void *kern, int nt, size_t smem, long long *resident) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void *, int, int, size_t>, long long> cache;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const auto key = std::make_tuple(kern, dev, nt, smem);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *resident = it->second;
+      return cudaSuccess;
+    }
+  }
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int sms = 0, occ = 0;
+  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, smem);
+  if (e != cudaSuccess) return e;
+  const long long r = (long long)sms * (occ > 0 ? occ : 1);
+  std::lock_guard<std::mutex> g(mu);
+  cache[key] = r;
+  *resident = r;
+  return cudaSuccess;
+}
+
+}  // namespace wl

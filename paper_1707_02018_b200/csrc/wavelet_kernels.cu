@@ -5,9 +5,7 @@
 // applied along axis 1 (rows) then axis 0 (columns); yhat = E y with E chosen per operator
 // (P:52-98):  W-dagger: E_bc;  W*: E_zpd / periodisation / (E_sym^dagger)* = E_sym diag(1/c)
 // (Eq. (4); reading R1).
-// Synthesis = exact transpose, written in gather form per axis: the extended-position sample
-//   u[t] = sum_{q < L/2} g[2q + 1 - (t & 1)] * c[floor(t/2) + q]
-// so one coefficient window feeds the output pair (t = 2s, 2s+1).
+// Synthesis (W) lives in synthesis_kernels.cu; the EDAG fold stays here.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -30,18 +28,6 @@ struct AnaParams {
   int ext;
   int chunk;  // coefficient rows per CTA
   int fast;   // 16-byte cp.async path allowed for interior chunks
-  T lo[kMaxL], hi[kMaxL];
-};
-
-template <typename T>
-struct SynParams {
-  const T *in[4];
-  long long in_pitch[4], in_bstride[4];
-  int m0, m1;
-  int coef_mod;
-  T *out;
-  long long out_pitch, out_bstride;
-  int N0, N1, o0, o1;
   T lo[kMaxL], hi[kMaxL];
 };
 
@@ -243,92 +229,6 @@ __global__ void __launch_bounds__(AnaCfg<T, L, TN, G>::NT, 2) k_analysis(const A
   }
 }
 
-// ----------------------------------------------------------------- synthesis
-template <typename T, int L, int TI, int TP>
-struct SynTile {
-  static constexpr int H = L / 2;
-  static constexpr int KR = TI / 2 + H - 1;
-  static constexpr int KC = TP / 2 + H - 1;
-  static constexpr int KCP = KC + 1;
-  static constexpr size_t smem_bytes() {
-    return sizeof(T) * (4 * (size_t)KR * KCP + 2 * (size_t)TI * KCP);
-  }
-};
-
-__device__ __forceinline__ int floor_div2(int t) { return t >> 1; }  // arithmetic shift = floor
-
-template <typename T, int L, int TI, int TP, int NT>
-__global__ void __launch_bounds__(NT) k_synthesis(const SynParams<T> p) {
-  using Tile = SynTile<T, L, TI, TP>;
-  constexpr int H = Tile::H, KR = Tile::KR, KC = Tile::KC, KCP = Tile::KCP;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T *cf = reinterpret_cast<T *>(smem_raw);  // [4][KR][KCP]
-  T *VL = cf + 4 * KR * KCP;                // [TI][KCP]
-  T *VH = VL + TI * KCP;
-
-  const int tid = threadIdx.x;
-  const int b = blockIdx.z;
-  // tiles cover extended positions t in [o, o+N) starting at an even t
-  const int T0 = 2 * floor_div2(p.o0) + blockIdx.y * TI;
-  const int P0 = 2 * floor_div2(p.o1) + blockIdx.x * TP;
-  const int kr0 = T0 / 2, kc0 = P0 / 2;  // T0, P0 even
-
-  for (int idx = tid; idx < 4 * KR * KC; idx += NT) {
-    int band = idx / (KR * KC);
-    int rem = idx - band * KR * KC;
-    int r = rem / KC, c = rem - r * KC;
-    int kr = kr0 + r, kc = kc0 + c;
-    T v = T(0);
-    if (p.coef_mod) {
-      kr %= p.m0; if (kr < 0) kr += p.m0;
-      kc %= p.m1; if (kc < 0) kc += p.m1;
-      v = p.in[band][(long long)b * p.in_bstride[band] + (long long)kr * p.in_pitch[band] + kc];
-    } else if (kr >= 0 && kr < p.m0 && kc >= 0 && kc < p.m1) {
-      v = p.in[band][(long long)b * p.in_bstride[band] + (long long)kr * p.in_pitch[band] + kc];
-    }
-    cf[(band * KR + r) * KCP + c] = v;
-  }
-  __syncthreads();
-  // axis 0: (LL, HL) -> VL ; (LH, HH) -> VH ; rows t = 2s (taps 2q+1) and 2s+1 (taps 2q)
-  const T *cLL = cf, *cLH = cf + KR * KCP, *cHL = cf + 2 * KR * KCP, *cHH = cf + 3 * KR * KCP;
-  for (int idx = tid; idx < (TI / 2) * KC; idx += NT) {
-    int s = idx / KC, c = idx - s * KC;
-    T eL = T(0), oL = T(0), eH = T(0), oH = T(0);
-#pragma unroll
-    for (int q = 0; q < H; q++) {
-      int o = (s + q) * KCP + c;
-      T a = cLL[o], d = cHL[o], a2 = cLH[o], d2 = cHH[o];
-      eL = fma(p.lo[2 * q + 1], a, fma(p.hi[2 * q + 1], d, eL));
-      oL = fma(p.lo[2 * q], a, fma(p.hi[2 * q], d, oL));
-      eH = fma(p.lo[2 * q + 1], a2, fma(p.hi[2 * q + 1], d2, eH));
-      oH = fma(p.lo[2 * q], a2, fma(p.hi[2 * q], d2, oH));
-    }
-    VL[(2 * s) * KCP + c] = eL;
-    VL[(2 * s + 1) * KCP + c] = oL;
-    VH[(2 * s) * KCP + c] = eH;
-    VH[(2 * s + 1) * KCP + c] = oH;
-  }
-  __syncthreads();
-  // axis 1
-  T *out = p.out + (long long)b * p.out_bstride;
-  for (int idx = tid; idx < TI * (TP / 2); idx += NT) {
-    int ii = idx / (TP / 2), s = idx - ii * (TP / 2);
-    T e = T(0), o = T(0);
-#pragma unroll
-    for (int q = 0; q < H; q++) {
-      T vL = VL[ii * KCP + s + q], vH = VH[ii * KCP + s + q];
-      e = fma(p.lo[2 * q + 1], vL, fma(p.hi[2 * q + 1], vH, e));
-      o = fma(p.lo[2 * q], vL, fma(p.hi[2 * q], vH, o));
-    }
-    int i = T0 + ii - p.o0;
-    int c0 = P0 + 2 * s - p.o1;
-    if (i >= 0 && i < p.N0) {
-      if (c0 >= 0 && c0 < p.N1) out[(long long)i * p.out_pitch + c0] = e;
-      if (c0 + 1 >= 0 && c0 + 1 < p.N1) out[(long long)i * p.out_pitch + c0 + 1] = o;
-    }
-  }
-}
-
 // ------------------------------------------------------------- EDAG fold
 template <typename T>
 __global__ void k_fold_sym_pinv(const T *__restrict__ U, long long upitch, long long ubs, T *__restrict__ y,
@@ -378,37 +278,11 @@ cudaError_t launch_analysis_t(const AnalysisArgs &a, cudaStream_t s) {
   p.chunk = chunk;
   size_t smem = C::smem_bytes();
   auto kern = k_analysis<T, L, TN, G>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  long long resident = 0;
+  cudaError_t e = kernel_resident(reinterpret_cast<const void *>(kern), C::NT, smem, &resident);
   if (e != cudaSuccess) return e;
   dim3 grid(strips, nchunk, a.batch);
   kern<<<grid, C::NT, smem, s>>>(p);
-  g_launches++;
-  return cudaGetLastError();
-}
-
-template <typename T, int L>
-cudaError_t launch_synthesis_t(const SynthesisArgs &a, cudaStream_t s) {
-  constexpr int TI = sizeof(T) == 4 ? 64 : 32;
-  constexpr int TP = TI, NT = 256;
-  using Tile = SynTile<T, L, TI, TP>;
-  SynParams<T> p;
-  for (int i = 0; i < 4; i++) {
-    p.in[i] = static_cast<const T *>(a.in[i]);
-    p.in_pitch[i] = a.in_pitch[i]; p.in_bstride[i] = a.in_bstride[i];
-  }
-  p.m0 = a.m0; p.m1 = a.m1; p.coef_mod = a.coef_mod;
-  p.out = static_cast<T *>(a.out);
-  p.out_pitch = a.out_pitch; p.out_bstride = a.out_bstride;
-  p.N0 = a.N0; p.N1 = a.N1; p.o0 = a.o0; p.o1 = a.o1;
-  for (int j = 0; j < kMaxL; j++) { p.lo[j] = T(j < L ? a.lo[j] : 0); p.hi[j] = T(j < L ? a.hi[j] : 0); }
-  size_t smem = Tile::smem_bytes();
-  auto kern = k_synthesis<T, L, TI, TP, NT>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  // extended span [o, o+N) starting from the even position 2*floor(o/2)
-  int span0 = a.o0 + a.N0 - 2 * (a.o0 >> 1), span1 = a.o1 + a.N1 - 2 * (a.o1 >> 1);
-  dim3 grid((span1 + TP - 1) / TP, (span0 + TI - 1) / TI, a.batch);
-  kern<<<grid, NT, smem, s>>>(p);
   g_launches++;
   return cudaGetLastError();
 }
@@ -425,28 +299,11 @@ cudaError_t dispatch_analysis(const AnalysisArgs &a, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
-template <typename T>
-cudaError_t dispatch_synthesis(const SynthesisArgs &a, cudaStream_t s) {
-  switch (a.L) {
-    case 2: return launch_synthesis_t<T, 2>(a, s);
-    case 4: return launch_synthesis_t<T, 4>(a, s);
-    case 8: return launch_synthesis_t<T, 8>(a, s);
-    case 10: return launch_synthesis_t<T, 10>(a, s);
-    case 16: return launch_synthesis_t<T, 16>(a, s);
-  }
-  return cudaErrorInvalidValue;
-}
-
 }  // namespace
 
 cudaError_t launch_analysis(int dtype, const AnalysisArgs &a, cudaStream_t s) {
   if (a.batch == 0 || a.m0 == 0 || a.m1 == 0) return cudaSuccess;
   return dtype == WL_F64 ? dispatch_analysis<double>(a, s) : dispatch_analysis<float>(a, s);
-}
-
-cudaError_t launch_synthesis(int dtype, const SynthesisArgs &a, cudaStream_t s) {
-  if (a.batch == 0 || a.N0 == 0 || a.N1 == 0) return cudaSuccess;
-  return dtype == WL_F64 ? dispatch_synthesis<double>(a, s) : dispatch_synthesis<float>(a, s);
 }
 
 cudaError_t launch_fold(int dtype, const FoldArgs &a, cudaStream_t s) {

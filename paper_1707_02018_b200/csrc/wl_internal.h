@@ -79,6 +79,18 @@ cudaError_t launch_blur(int dtype, const BlurArgs &a, cudaStream_t s);
 cudaError_t launch_blur_residual(int dtype, const BlurArgs &a, cudaStream_t s);
 cudaError_t launch_zero(void *ptr, size_t bytes, cudaStream_t s);
 
+// Encode a 3-D tiled TMA descriptor (CUtensorMap, 128 bytes at `map`) over a tensor of
+// d0 x d1 x d2 elements of `elem_bytes` (4: fp32, 8: fp64) with byte strides s1 (dim 1) and
+// s2 (dim 2), box (box0, box1, 1), no swizzle, zero out-of-bounds fill.  Returns false if
+// the driver entry point is unavailable or the layout is not TMA-legal (16-byte strides...).
+bool encode_tmap_3d(void *map, int elem_bytes, const void *base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
+                    uint64_t s2, uint32_t box0, uint32_t box1);
+
+// Opt `kern` into `smem` bytes of dynamic shared memory and return the number of CTAs of
+// `nt` threads the current device keeps resident (SMs x CTAs per SM).  Cached per (kernel,
+// device), so a launch pays the attribute / occupancy queries once.
+cudaError_t kernel_resident(const void *kern, int nt, size_t smem, long long *resident);
+
 }  // namespace wl
 
 struct wl_plan {
