@@ -1,0 +1,336 @@
+// W* and W-dagger: one 2-D level of the wavelet analysis (sm_100a), streaming column-strip kernel.
+//
+// Analysis core (reading R5):  out[k] = sum_{j<L} f[j] * yhat[2k+1-j],
+// applied along axis 1 (rows) then axis 0 (columns); yhat = E y with E chosen per operator
+// (P:52-98):  W-dagger: E_bc;  W*: E_zpd / periodisation / (E_sym^dagger)* = E_sym diag(1/c)
+// (Eq. (4); reading R1).  Subband XY = axis-0 filter X, axis-1 filter Y.
+//
+// A CTA owns TQ coefficient columns of one image and a band of coefficient rows; it walks
+// down the input rows 2G at a time (G coefficient rows out per iteration):
+//   A  the 2G input rows of the strip's window (2TQ + L - 2 columns) land in a double
+//      buffer: one TMA box issued by one thread and completed on an mbarrier when the
+//      extension is the zero extension (TMA's zero fill) or the block lies inside the image;
+//      otherwise (symmetric / periodic / EDAG-weighted edges) they are gathered with the
+//      extension map by cp.async / per-element loads;
+//   B  axis-1 pass: every input row -> (lo, hi) coefficient pairs with FFMA2 on the tap pair
+//      (f_lo[j], f_hi[j]) against a broadcast sample, into the lo / hi row histories
+//      (L-2 carried rows + 2G new);
+//   C  axis-0 pass: each thread owns a column pair of one history and produces VC coefficient
+//      rows of two subbands (X = lo, hi) from a register window, stored as float2 pairs
+//      (padding columns of the pitched rows written as 0).
+// Loops run tap-outer so only one tap pair is live at a time (no register spills).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include "device_common.cuh"
+#include "wl_internal.h"
+
+namespace wl {
+namespace {
+
+// Source index of extended position t (or -1 for a zero) and its weight.
+template <typename T>
+__device__ __forceinline__ int ext_src(int t, int n, int ext, int Lp, T &w) {
+  w = T(1);
+  if (ext == EXT_ZERO) return (t >= 0 && t < n) ? t : -1;
+  if (ext == EXT_PER) {
+    int r = t % n;
+    return r < 0 ? r + n : r;
+  }
+  int s = t < 0 ? -1 - t : (t >= n ? 2 * n - 1 - t : t);
+  if (s < 0 || s >= n) return -1;  // only reached by positions that feed no stored output
+  if (ext == EXT_SYM_PADJ) {
+    // multiplicity c_s = #{t in [-Lp, n+Lp) : src(t) = s} = 1 + [s < Lp] + [s >= n - Lp]
+    int c = 1 + (s < Lp ? 1 : 0) + (s >= n - Lp ? 1 : 0);
+    w = T(1) / T(c);
+  }
+  return s;
+}
+
+template <typename T, int L>
+struct ACfg {
+  using P = typename Pair<T>::t;
+  static constexpr int VEC = Vec16<T>::n;
+  static constexpr int TQ = sizeof(T) == 4 ? 64 : 32;   // coefficient columns per strip
+  static constexpr int G = 16;                           // coefficient rows per iteration
+  static constexpr int GI = 2 * G;                       // input rows per iteration
+  static constexpr int V = 8;                            // coefficient outputs per B item
+  static constexpr int VC = 4;                           // coefficient rows per C item
+  static constexpr int SHIFT = ((2 - L) % VEC + VEC) % VEC;  // box column of input column 2q0+2-L
+  static constexpr int UW = round_up_c(SHIFT + 2 * TQ + L - 2, VEC);  // input box width
+  static constexpr int UP = UW;                          // dense TMA box rows
+  static constexpr int NV = UW / VEC;
+  static constexpr int NWB = round_up_c(SHIFT + 2 * V + L - 2, VEC);  // B window
+  static constexpr int SEGB = TQ / V;
+  static constexpr int HR = L - 2 + GI;                  // history rows (L-2 carried + 2G new)
+  static constexpr int HP = conflict_free_pitch<T>(TQ);
+  static_assert(2 * V * (SEGB - 1) + NWB <= UW, "B window overruns the input row");
+  static_assert(GI >= L - 2, "history move must not overlap");
+  static constexpr int ITEMS_B = SEGB * GI;
+  static constexpr int ITEMS_C = 2 * (TQ / 2) * (G / VC);
+  static constexpr int NT = round_up_c(std::max(ITEMS_B, ITEMS_C), 32);
+  static constexpr size_t OFF_U = 0;  // [2][GI][UP]
+  static constexpr size_t OFF_H = OFF_U + round_up_c(2 * GI * UP * (int)sizeof(T), 128);  // [2 sets][HR][HP]
+  static constexpr size_t OFF_BAR = OFF_H + 2 * (size_t)HR * HP * sizeof(T);
+  static constexpr size_t smem_bytes() { return OFF_BAR + 2 * sizeof(uint64_t); }
+};
+
+template <typename T, int L>
+struct AnaStreamParams {
+  using P = typename Pair<T>::t;
+  CUtensorMap tmap;          // input: box (UW, GI, 1)   (valid if tma)
+  const T *in;
+  long long in_pitch, in_bstride;
+  int n0, n1;
+  T *out[4];                 // LL, LH, HL, HH
+  long long out_pitch[4], out_bstride[4];
+  int m0, m1, ext, tma, tma_any_block, fast;
+  int nstrips;
+  RunMap runs;               // (image, strip) columns x bands of coefficient rows
+  T flo[L], fhi[L];          // raw taps (gather weights)
+  P fb[L];                   // B tap pairs (f_lo[j], f_hi[j])
+  P slo[L], shi[L];          // C broadcast taps (f[j], f[j])
+};
+
+template <typename T, int L>
+__global__ void __launch_bounds__(ACfg<T, L>::NT, sizeof(T) == 4 ? 3 : 1)
+    k_ana_stream(const __grid_constant__ AnaStreamParams<T, L> p) {
+  using C = ACfg<T, L>;
+  using P = typename C::P;
+  using Vt = typename Vec16<T>::type;
+  constexpr int G = C::G, GI = C::GI, VEC = C::VEC, V = C::V, VC = C::VC, TQ = C::TQ;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T *ubuf = reinterpret_cast<T *>(smem_raw + C::OFF_U);  // [2][GI][UP] input rows
+  T *hist = reinterpret_cast<T *>(smem_raw + C::OFF_H);  // [2][HR][HP] lo / hi coefficient columns
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + C::OFF_BAR);
+
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+  }
+  __syncthreads();
+  unsigned phase = 0;
+  // B item: segment fastest; C item: column pair fastest, then set (lo / hi), then group
+  const bool actB = tid < C::ITEMS_B;
+  const int segB = tid % C::SEGB, rowB = tid / C::SEGB;
+  const bool actC = tid < C::ITEMS_C;
+  const int mC = tid % (TQ / 2), setC = (tid / (TQ / 2)) & 1, grpC = tid / TQ;
+
+  const int nruns = p.runs.nruns();
+  for (int run = blockIdx.x; run < nruns; run += gridDim.x) {
+    int col, kr0, kr1;
+    p.runs.get(run, col, kr0, kr1);
+    if (kr0 >= kr1) continue;  // (uniform) empty trailing band
+    const int img = col / p.nstrips, strip = col - img * p.nstrips;
+    const int q0 = strip * TQ;
+    const int cbox = 2 * q0 + 2 - L - C::SHIFT;  // input column of box column 0 (VEC aligned)
+    const T *in = p.in + (long long)img * p.in_bstride;
+    const int nblk = (kr1 - kr0 + G - 1) / G;
+    // C output columns q = q0 + 2 mC (+1) of subbands (setC: LL/HL from lo, LH/HH from hi)
+    const int qc = q0 + 2 * mC;
+    T *oX0 = p.out[setC] + (long long)img * p.out_bstride[setC];          // X = lo: LL or LH
+    T *oX1 = p.out[setC + 2] + (long long)img * p.out_bstride[setC + 2];  // X = hi: HL or HH
+    const long long pX0 = p.out_pitch[setC], pX1 = p.out_pitch[setC + 2];
+
+    // input block b (b = -1 .. nblk-1): rows 2(kr0 + bG) .. +2G -> ubuf[b & 1]
+    auto load_block = [&](int b) -> bool {
+      const int r_in = 2 * (kr0 + b * G);
+      T *dst0 = ubuf + (b & 1) * GI * C::UP;
+      const bool inside = r_in >= 0 && r_in + GI <= p.n0 && cbox >= 0 && cbox + C::UW <= p.n1;
+      if (p.tma && (p.tma_any_block || inside)) {
+        if (tid == 0) {
+          fence_proxy_async();
+          mbar_arrive_expect_tx(bar + (b & 1), GI * C::UW * sizeof(T));
+          tma_load_3d(dst0, &p.tmap, bar + (b & 1), cbox, r_in, img);
+        }
+        return true;
+      }
+      for (int idx = tid; idx < GI * C::NV; idx += C::NT) {
+        const int r = idx / C::NV, v = idx - r * C::NV;
+        T wr;
+        const int sr = ext_src<T>(r_in + r, p.n0, p.ext, L - 1, wr);
+        T *dst = dst0 + r * C::UP + v * VEC;
+        const int cg = cbox + v * VEC;
+        if (sr < 0) {
+          T z[VEC];
+#pragma unroll
+          for (int u = 0; u < VEC; u++) z[u] = T(0);
+          *reinterpret_cast<Vt *>(dst) = vec_make<T>(z);
+        } else if (p.fast && p.ext != EXT_SYM_PADJ && cg >= 0 && cg + VEC <= p.n1) {
+          cp_async16(dst, in + (long long)sr * p.in_pitch + cg);
+        } else {
+          T z[VEC];
+#pragma unroll
+          for (int u = 0; u < VEC; u++) {
+            T wc;
+            const int sc = ext_src<T>(cg + u, p.n1, p.ext, L - 1, wc);
+            z[u] = sc >= 0 ? in[(long long)sr * p.in_pitch + sc] * (wr * wc) : T(0);
+          }
+          *reinterpret_cast<Vt *>(dst) = vec_make<T>(z);
+        }
+      }
+      return false;
+    };
+
+    __syncthreads();  // previous run's readers are done
+    bool armed = load_block(-1);
+    cp_async_commit();
+    for (int it = -1; it < nblk; it++) {
+      const int slot = it & 1;
+      cp_async_wait_all();
+      if (armed) {
+        mbar_wait(bar + slot, (phase >> slot) & 1);
+        phase ^= 1u << slot;
+      }
+      __syncthreads();  // (1) block it landed; the history move of it-1 is done
+      armed = (it + 1 < nblk) ? load_block(it + 1) : false;
+      cp_async_commit();
+      // B: input row rowB of the block -> lo/hi history row L-2+rowB, coefficient columns V*segB ..
+      if (actB) {
+        const T *src = ubuf + (slot * GI + rowB) * C::UP + 2 * V * segB;
+        T win[C::NWB];
+#pragma unroll
+        for (int i = 0; i < C::NWB / VEC; i++) vec_split<T>(reinterpret_cast<const Vt *>(src)[i], win + i * VEC);
+        P acc[V];
+#pragma unroll
+        for (int k = 0; k < V; k++) acc[k] = zero2<P>();
+#pragma unroll
+        for (int j = 0; j < L; j++) {  // tap-outer
+          const P f = p.fb[j];
+#pragma unroll
+          for (int k = 0; k < V; k++) acc[k] = fma2(f, splat2<P>(win[C::SHIFT + 2 * k + L - 1 - j]), acc[k]);
+        }
+        T lo[V], hi[V];
+#pragma unroll
+        for (int k = 0; k < V; k++) {
+          lo[k] = acc[k].x;
+          hi[k] = acc[k].y;
+        }
+        Vt *dl = reinterpret_cast<Vt *>(hist + (L - 2 + rowB) * C::HP + V * segB);
+        Vt *dh = reinterpret_cast<Vt *>(hist + (C::HR + L - 2 + rowB) * C::HP + V * segB);
+#pragma unroll
+        for (int i = 0; i < V / VEC; i++) {
+          dl[i] = vec_make<T>(lo + i * VEC);
+          dh[i] = vec_make<T>(hi + i * VEC);
+        }
+      }
+      __syncthreads();  // (2)
+      // C: coefficient rows kr = kr0 + it*G + grpC*VC + v (history rows 2(grpC*VC+v) + L-1-j)
+      if (actC && it >= 0) {
+        const int krb = kr0 + it * G + grpC * VC;
+        const T *hs = hist + setC * C::HR * C::HP + (2 * grpC * VC) * C::HP + 2 * mC;
+        P win[2 * VC + L - 2];
+#pragma unroll
+        for (int i = 0; i < 2 * VC + L - 2; i++) win[i] = *reinterpret_cast<const P *>(hs + i * C::HP);
+        P a0[VC], a1[VC];
+#pragma unroll
+        for (int v = 0; v < VC; v++) a0[v] = a1[v] = zero2<P>();
+#pragma unroll
+        for (int j = 0; j < L; j++) {
+          const P fl = p.slo[j], fh = p.shi[j];
+#pragma unroll
+          for (int v = 0; v < VC; v++) {
+            a0[v] = fma2(fl, win[2 * v + L - 1 - j], a0[v]);
+            a1[v] = fma2(fh, win[2 * v + L - 1 - j], a1[v]);
+          }
+        }
+        // pitched rows: columns [m1, pitch) are padding written as 0; qc is even and so is
+        // every pitch, so a pair never straddles the pitch
+        const bool in0 = qc < p.m1, in1 = qc + 1 < p.m1;
+        const bool st0 = qc < pX0;
+#pragma unroll
+        for (int v = 0; v < VC; v++) {
+          const int kr = krb + v;
+          if (kr >= kr1 || !st0) continue;
+          P z0 = a0[v], z1 = a1[v];
+          if (!in0) z0.x = z1.x = T(0);
+          if (!in1) z0.y = z1.y = T(0);
+          *reinterpret_cast<P *>(oX0 + (long long)kr * pX0 + qc) = z0;
+          *reinterpret_cast<P *>(oX1 + (long long)kr * pX1 + qc) = z1;
+        }
+      }
+      __syncthreads();  // (3) history readers done
+      // carry history rows [GI, GI+L-2) to [0, L-2) in both sets
+      constexpr int CPR = TQ / VEC;
+      for (int idx = tid; idx < 2 * (L - 2) * CPR; idx += C::NT) {
+        const int set = idx / ((L - 2) * CPR), rem = idx - set * (L - 2) * CPR;
+        const int r = rem / CPR, c = rem - r * CPR;
+        T *hb = hist + set * C::HR * C::HP;
+        *reinterpret_cast<Vt *>(hb + r * C::HP + c * VEC) = *reinterpret_cast<const Vt *>(hb + (r + GI) * C::HP + c * VEC);
+      }
+    }
+    cp_async_wait_all();
+  }
+}
+
+template <typename T, int L>
+cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
+  using C = ACfg<T, L>;
+  AnaStreamParams<T, L> p;
+  memset(&p, 0, sizeof p);
+  p.in = static_cast<const T *>(a.in);
+  p.in_pitch = a.in_pitch;
+  p.in_bstride = a.in_bstride;
+  p.n0 = a.n0;
+  p.n1 = a.n1;
+  for (int i = 0; i < 4; i++) {
+    p.out[i] = static_cast<T *>(a.out[i]);
+    p.out_pitch[i] = a.out_pitch[i];
+    p.out_bstride[i] = a.out_bstride[i];
+  }
+  p.m0 = a.m0;
+  p.m1 = a.m1;
+  p.ext = a.ext;
+  p.fast = (a.in_pitch % C::VEC == 0) && (a.in_bstride % C::VEC == 0) && (reinterpret_cast<uintptr_t>(a.in) % 16 == 0);
+  bool tma = p.fast && !getenv("WL_NO_TMA") && a.ext != EXT_SYM_PADJ;
+  if (tma)
+    tma = encode_tmap_3d(&p.tmap, sizeof(T), a.in, (uint64_t)a.n1, (uint64_t)a.n0, (uint64_t)a.batch,
+                         (uint64_t)a.in_pitch * sizeof(T), (uint64_t)a.in_bstride * sizeof(T), C::UW, C::GI);
+  p.tma = tma;
+  p.tma_any_block = a.ext == EXT_ZERO;  // TMA's zero fill is the zero extension
+  for (int j = 0; j < L; j++) {
+    p.flo[j] = T(a.lo[j]);
+    p.fhi[j] = T(a.hi[j]);
+    p.fb[j].x = T(a.lo[j]);
+    p.fb[j].y = T(a.hi[j]);
+    p.slo[j].x = p.slo[j].y = T(a.lo[j]);
+    p.shi[j].x = p.shi[j].y = T(a.hi[j]);
+  }
+  p.nstrips = (a.m1 + C::TQ - 1) / C::TQ;
+  const size_t smem = C::smem_bytes();
+  auto kern = k_ana_stream<T, L>;
+  long long resident = 0;
+  cudaError_t e = kernel_resident(reinterpret_cast<const void *>(kern), C::NT, smem, &resident);
+  if (e != cudaSuccess) return e;
+  p.runs = RunMap::make((long long)a.batch * p.nstrips, a.m0, resident, C::G, 1);
+  const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
+  kern<<<grid, C::NT, smem, s>>>(p);
+  g_launches++;
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t dispatch(const AnalysisArgs &a, cudaStream_t s) {
+  switch (a.L) {
+    case 2: return launch_ana_stream_t<T, 2>(a, s);
+    case 4: return launch_ana_stream_t<T, 4>(a, s);
+    case 8: return launch_ana_stream_t<T, 8>(a, s);
+    case 10: return launch_ana_stream_t<T, 10>(a, s);
+    case 16: return launch_ana_stream_t<T, 16>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+cudaError_t launch_analysis(int dtype, const AnalysisArgs &a, cudaStream_t s) {
+  if (a.batch == 0 || a.m0 == 0 || a.m1 == 0) return cudaSuccess;
+  return dtype == WL_F64 ? dispatch<double>(a, s) : dispatch<float>(a, s);
+}
+
+}  // namespace wl

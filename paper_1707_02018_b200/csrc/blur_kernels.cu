@@ -129,29 +129,31 @@ struct BlurStreamParams {
 template <typename T, int HW, int V, int OFF, int NW>
 __device__ __forceinline__ void hpass_win(const T *win, const BlurStreamParams<T, HW> &p, T *outv) {
   using P = typename Pair<T>::t;
+  // tap-outer: only the (even, odd) tap pairs of one m are live at a time.  The partner of an
+  // out-of-range tap is a real window sample times a zero coefficient (no zero moves).
+  P acc[V];
 #pragma unroll
-  for (int j = 0; j < V; j++) {
-    const int s = j + OFF;
-    P acc = zero2<P>();
-    if (s % 2 == 0) {
+  for (int j = 0; j < V; j++) acc[j] = zero2<P>();
 #pragma unroll
-      for (int m = 0; m <= HW; m++) {
-        P x;
+  for (int m = 0; m <= HW; m++) {
+    const P ce = p.ce[m], co = p.co[m];
+#pragma unroll
+    for (int j = 0; j < V; j++) {
+      const int s = j + OFF;
+      P x;
+      if (s % 2 == 0) {
         x.x = win[s + 2 * m];
-        x.y = (2 * m + 1 <= 2 * HW) ? win[s + 2 * m + 1] : T(0);
-        acc = fma2(p.ce[m], x, acc);
-      }
-    } else {
-#pragma unroll
-      for (int m = 0; m <= HW; m++) {
-        P x;
-        x.x = (m > 0) ? win[s - 1 + 2 * m] : T(0);
+        x.y = (s + 2 * m + 1 < NW) ? win[s + 2 * m + 1] : T(0);
+        acc[j] = fma2(ce, x, acc[j]);
+      } else {
+        x.x = win[s - 1 + 2 * m];
         x.y = win[s + 2 * m];
-        acc = fma2(p.co[m], x, acc);
+        acc[j] = fma2(co, x, acc[j]);
       }
     }
-    outv[j] = acc.x + acc.y;
   }
+#pragma unroll
+  for (int j = 0; j < V; j++) outv[j] = acc[j].x + acc[j].y;
 }
 
 // Window of a horizontal item: NW samples starting at frame column `fc` of `srow`.  Away
@@ -183,15 +185,21 @@ __device__ __forceinline__ void vpass(const T *src, const BlurStreamParams<T, HW
   P win[VC + 2 * HW];
 #pragma unroll
   for (int i = 0; i < VC + 2 * HW; i++) win[i] = *reinterpret_cast<const P *>(src + i * PITCH);
+  // tap-outer, two independent chains (even / odd taps) per output
+  P a[VC], b[VC];
 #pragma unroll
-  for (int v = 0; v < VC; v++) {  // two independent chains (even / odd taps) per output
-    P a = zero2<P>(), b = zero2<P>();
+  for (int v = 0; v < VC; v++) a[v] = b[v] = zero2<P>();
 #pragma unroll
-    for (int d = 0; d < 2 * HW + 1; d += 2) a = fma2(p.cc[d], win[v + d], a);
+  for (int d = 0; d < 2 * HW + 1; d++) {
+    const P c = p.cc[d];
 #pragma unroll
-    for (int d = 1; d < 2 * HW + 1; d += 2) b = fma2(p.cc[d], win[v + d], b);
-    acc[v] = add2(a, b);
+    for (int v = 0; v < VC; v++) {
+      if (d % 2 == 0) a[v] = fma2(c, win[v + d], a[v]);
+      else b[v] = fma2(c, win[v + d], b[v]);
+    }
   }
+#pragma unroll
+  for (int v = 0; v < VC; v++) acc[v] = add2(a[v], b[v]);
 }
 
 template <typename T>

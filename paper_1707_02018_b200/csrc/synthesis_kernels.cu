@@ -327,7 +327,7 @@ cudaError_t launch_synth_stream_t(const SynthesisArgs &a, cudaStream_t s) {
   cudaError_t e = kernel_resident(reinterpret_cast<const void *>(kern), C::NT, smem, &resident);
   if (e != cudaSuccess) return e;
   // one run per resident CTA when the columns allow it; even bands of >= 4 iterations
-  p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident, 8 * C::G, 2);
+  p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident, 2 * C::G, 2);
   const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
   kern<<<grid, C::NT, smem, s>>>(p);
   g_launches++;
