@@ -110,33 +110,28 @@ class ClockSampler:
 
 
 def dist_setup():
+    """One process per GPU (torchrun env); the process group only brackets the timed region."""
     import torch
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if ws > 1:
+
+    from paper_1707_02018_b200 import replicas
+    info = replicas.rank_info()
+    if info.world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(info.local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", info.local))
     else:
         torch.cuda.set_device(0)
-    return ws, rank, local
+    return info.world, info.rank, info.local
 
 
 def barrier(ws):
-    if ws > 1:
-        import torch.distributed as dist
-        dist.barrier()
+    from paper_1707_02018_b200 import replicas
+    replicas.barrier(ws)
 
 
 def max_over_ranks(v, ws):
-    if ws == 1:
-        return v
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    from paper_1707_02018_b200 import replicas
+    return replicas.max_over_ranks(v, ws)
 
 
 def time_calls(torch, fn, reps, warmup=3):

@@ -114,6 +114,8 @@ __global__ void __launch_bounds__(ACfg<T, L>::NT, sizeof(T) == 4 ? 3 : 1)
     mbar_init(bar + 1, 1);
   }
   __syncthreads();
+  pdl_launch_dependents();
+  pdl_wait();  // the previous kernel of the stream wrote our inputs
   unsigned phase = 0;
   // B item: segment fastest; C item: column pair fastest, then set (lo / hi), then group
   const bool actB = tid < C::ITEMS_B;
@@ -309,8 +311,9 @@ cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   p.runs = RunMap::make((long long)a.batch * p.nstrips, a.m0, resident, C::G, 1);
   const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
-  kern<<<grid, C::NT, smem, s>>>(p);
+  e = launch_pdl(kern, grid, C::NT, smem, s, p);
   g_launches++;
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

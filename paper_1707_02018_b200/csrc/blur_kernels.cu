@@ -240,6 +240,8 @@ __global__ void __launch_bounds__(BCfg<T, HW, RESID>::NT, (sizeof(T) == 4 && BCf
     mbar_init(bar + 1, 1);
   }
   __syncthreads();
+  pdl_launch_dependents();
+  pdl_wait();  // the previous kernel of the stream wrote our inputs
   unsigned phase = 0;  // parity of the completed phases of bar[0] (bit 0) and bar[1] (bit 1)
 
   // per-thread work items of every stage (fixed for the whole kernel)
@@ -494,8 +496,9 @@ cudaError_t launch_stream(const BlurArgs &a, cudaStream_t s) {
     e = cudaMemsetAsync(a.f, 0, sizeof(double) * (size_t)a.batch, s);
     if (e != cudaSuccess) return e;
   }
-  kern<<<grid, C::NT, smem, s>>>(p);
+  e = launch_pdl(kern, grid, C::NT, smem, s, p);
   g_launches++;
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

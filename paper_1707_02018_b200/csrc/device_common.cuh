@@ -117,6 +117,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
+// Programmatic dependent launch: let the next kernel in the stream start its prologue now;
+// wait until the previous kernel's results are visible before touching global memory.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 // Order this thread's earlier generic-proxy shared-memory accesses before later async-proxy
 // (TMA) accesses of the same buffers.
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }

@@ -101,6 +101,8 @@ __global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 3 : 1)
     mbar_init(bar + 1, 1);
   }
   __syncthreads();
+  pdl_launch_dependents();
+  pdl_wait();  // the previous kernel of the stream wrote our inputs
   unsigned phase = 0;
   // S1 item: segment fastest; S0 item: column pair fastest
   const bool act1 = tid < C::ITEMS1;
@@ -329,8 +331,9 @@ cudaError_t launch_synth_stream_t(const SynthesisArgs &a, cudaStream_t s) {
   // one run per resident CTA when the columns allow it; even bands of >= 4 iterations
   p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident, 2 * C::G, 2);
   const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
-  kern<<<grid, C::NT, smem, s>>>(p);
+  e = launch_pdl(kern, grid, C::NT, smem, s, p);
   g_launches++;
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -91,6 +91,24 @@ bool encode_tmap_3d(void *map, int elem_bytes, const void *base, uint64_t d0, ui
 // device), so a launch pays the attribute / occupancy queries once.
 cudaError_t kernel_resident(const void *kern, int nt, size_t smem, long long *resident);
 
+// Launch with programmatic stream serialization (PDL): the kernel may start while the
+// previous kernel of the stream drains; it must call pdl_wait() before its first global
+// memory access (every streaming kernel of libwl does, right after its shared-memory setup).
+template <typename Kern, typename Params>
+cudaError_t launch_pdl(Kern kern, int grid, int nt, size_t smem, cudaStream_t s, const Params &p) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)nt);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
 }  // namespace wl
 
 struct wl_plan {

@@ -1,6 +1,6 @@
 #!/bin/bash
 # One GPU session: parity tests, smoke, microbench, bench, ncu launch list + full capture of the top kernel.
-# usage (under gpurun): bash tools/gpu_check.sh [kernel-regex]
+# usage (under gpurun): bash tools/gpu_check.sh [kernel-regex[,kernel-regex...]]
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 K=${1:-blur_residual}
@@ -18,5 +18,7 @@ CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
 if [ -z "$NONCU" ]; then
   timeout 600 $CMD > gpurun_out/plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1; echo "ncu launches rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 2 -c 1 -o gpurun_out/prof_$K -f $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+  for KK in $(echo $K | tr ',' ' '); do
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:$KK -s 2 -c 1 -o gpurun_out/prof_$KK -f $CMD > gpurun_out/ncu_full_$KK.log 2>&1; echo "ncu full $KK rc=$?"
+  done
 fi
