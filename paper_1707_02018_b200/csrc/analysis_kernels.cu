@@ -56,7 +56,10 @@ struct ACfg {
   using P = typename Pair<T>::t;
   static constexpr int VEC = Vec16<T>::n;
   static constexpr int TQ = sizeof(T) == 4 ? 64 : 32;   // coefficient columns per strip
-  static constexpr int G = 16;                           // coefficient rows per iteration
+#ifndef WL_ANA_G
+#define WL_ANA_G 8  // A/B on B200: 8 beat 16 at cfg5 (-10 us), equal at cfg4
+#endif
+  static constexpr int G = WL_ANA_G;                     // coefficient rows per iteration
   static constexpr int GI = 2 * G;                       // input rows per iteration
   static constexpr int V = 8;                            // coefficient outputs per B item
   static constexpr int VC = 4;                           // coefficient rows per C item
@@ -97,7 +100,7 @@ struct AnaStreamParams {
 };
 
 template <typename T, int L>
-__global__ void __launch_bounds__(ACfg<T, L>::NT, sizeof(T) == 4 ? 3 : 1)
+__global__ void __launch_bounds__(ACfg<T, L>::NT, sizeof(T) == 4 ? 768 / ACfg<T, L>::NT : 1)
     k_ana_stream(const __grid_constant__ AnaStreamParams<T, L> p) {
   using C = ACfg<T, L>;
   using P = typename C::P;
@@ -245,6 +248,15 @@ __global__ void __launch_bounds__(ACfg<T, L>::NT, sizeof(T) == 4 ? 3 : 1)
         // every pitch, so a pair never straddles the pitch
         const bool in0 = qc < p.m1, in1 = qc + 1 < p.m1;
         const bool st0 = qc < pX0;
+        if (in1 && krb + VC <= kr1) {  // fast path: whole item inside the band and the image
+          T *d0 = oX0 + (long long)krb * pX0 + qc;
+          T *d1 = oX1 + (long long)krb * pX1 + qc;
+#pragma unroll
+          for (int v = 0; v < VC; v++) {
+            *reinterpret_cast<P *>(d0 + v * pX0) = a0[v];
+            *reinterpret_cast<P *>(d1 + v * pX1) = a1[v];
+          }
+        } else
 #pragma unroll
         for (int v = 0; v < VC; v++) {
           const int kr = krb + v;

@@ -180,15 +180,20 @@ __device__ __forceinline__ void load_window(T *win, const T *srow, int fc, bool 
 
 // Vertical pass over a column pair: VC outputs from VC + 2HW consecutive rows at `src` (pitch).
 template <typename T, int HW, int VC, int PITCH>
-__device__ __forceinline__ void vpass(const T *src, const BlurStreamParams<T, HW> &p, typename Pair<T>::t *acc) {
+__device__ __forceinline__ void vpass(const T *src, const BlurStreamParams<T, HW> &p, typename Pair<T>::t *acc,
+                                      const typename Pair<T>::t *init = nullptr) {
   using P = typename Pair<T>::t;
   P win[VC + 2 * HW];
 #pragma unroll
   for (int i = 0; i < VC + 2 * HW; i++) win[i] = *reinterpret_cast<const P *>(src + i * PITCH);
-  // tap-outer, two independent chains (even / odd taps) per output
+  // tap-outer, two independent chains (even / odd taps) per output; the even chain starts
+  // at `init` (the residual's -b) when given
   P a[VC], b[VC];
 #pragma unroll
-  for (int v = 0; v < VC; v++) a[v] = b[v] = zero2<P>();
+  for (int v = 0; v < VC; v++) {
+    a[v] = init ? init[v] : zero2<P>();
+    b[v] = zero2<P>();
+  }
 #pragma unroll
   for (int d = 0; d < 2 * HW + 1; d++) {
     const P c = p.cc[d];
@@ -287,7 +292,7 @@ __global__ void __launch_bounds__(BCfg<T, HW, RESID>::NT, (sizeof(T) == 4 && BCf
     const int colD = c0 + 2 * mD;
     const bool actD = actD0 && colD < p.w;
     const bool ovecD = p.fast && colD + 1 < p.w;
-    double fsum = 0.0;
+    double fsx = 0.0, fsy = 0.0;  // per-column sums of r^2 (masked to the tile at the end)
 
     // batch k: u rows e_begin + kG .. and (residual) b rows e_begin + kG - HW .. -> slot k & 1.
     // Returns whether the batch armed its barrier.
@@ -379,20 +384,29 @@ __global__ void __launch_bounds__(BCfg<T, HW, RESID>::NT, (sizeof(T) == 4 && BCf
       if (actC) {
         const int xb = e - HW + grpC * VC;
         P acc[VC];
-        vpass<T, HW, VC, C::H1P>(h1 + grpC * VC * C::H1P + 2 * mC, p, acc);
         if (RESID) {
-          // f sums r^2 over the item's valid rows; the tile column mask is applied once
+          // r = V h1 - b (the chain starts at -b); f sums r^2 over the item's valid rows per
+          // column, the tile column mask is applied once per run
+          P *rb = reinterpret_cast<P *>(bbuf + ((it & 1) * G + grpC * VC) * C::BP + 2 * mC);
+          P nb[VC];
+#pragma unroll
+          for (int v = 0; v < VC; v++) {
+            const P bv = rb[v * (C::BP / 2)];
+            nb[v].x = -bv.x;
+            nb[v].y = -bv.y;
+          }
+          vpass<T, HW, VC, C::H1P>(h1 + grpC * VC * C::H1P + 2 * mC, p, acc, nb);
           P fa = zero2<P>();
           const bool rows_in = xb >= r0 && xb + VC <= r1;
 #pragma unroll
           for (int v = 0; v < VC; v++) {
-            P *rb = reinterpret_cast<P *>(bbuf + ((it & 1) * G + grpC * VC + v) * C::BP + 2 * mC);
-            const P r = sub2(acc[v], *rb);
-            *rb = r;
-            if (rows_in || (xb + v >= r0 && xb + v < r1)) fa = fma2(r, r, fa);
+            rb[v * (C::BP / 2)] = acc[v];
+            if (rows_in || (xb + v >= r0 && xb + v < r1)) fa = fma2(acc[v], acc[v], fa);
           }
-          fsum += (double)(fa.x * fmask.x) + (double)(fa.y * fmask.y);
+          fsx += (double)fa.x;
+          fsy += (double)fa.y;
         } else {
+          vpass<T, HW, VC, C::H1P>(h1 + grpC * VC * C::H1P + 2 * mC, p, acc);
 #pragma unroll
           for (int v = 0; v < VC; v++) {
             const int x = xb + v;
@@ -438,6 +452,7 @@ __global__ void __launch_bounds__(BCfg<T, HW, RESID>::NT, (sizeof(T) == 4 && BCf
     }
     cp_async_wait_all();
     if (RESID && p.f) {
+      double fsum = fsx * (double)fmask.x + fsy * (double)fmask.y;
       for (int o = 16; o > 0; o >>= 1) fsum += __shfl_xor_sync(0xffffffffu, fsum, o);
       if ((tid & 31) == 0) red[tid >> 5] = fsum;
       __syncthreads();

@@ -42,7 +42,10 @@ struct SCfg {
   static constexpr int VEC = Vec16<T>::n;
   static constexpr int H = L / 2;
   static constexpr int TW = sizeof(T) == 4 ? 128 : 64;  // extended output columns per strip (even)
-  static constexpr int G = 16;                           // coefficient rows per iteration
+#ifndef WL_SYN_G
+#define WL_SYN_G 16
+#endif
+  static constexpr int G = WL_SYN_G;                     // coefficient rows per iteration
   static constexpr int SP = 8;                           // output column pairs per S1 item
   static constexpr int VC = 4;                           // s-values (output row pairs) per S0 item
   static constexpr int KCW = round_up_c(TW / 2 + H - 1, VEC);  // coefficient columns loaded
@@ -83,7 +86,7 @@ struct SynStreamParams {
 };
 
 template <typename T, int L>
-__global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 3 : 1)
+__global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 768 / SCfg<T, L>::NT : 1)
     k_synth_stream(const __grid_constant__ SynStreamParams<T, L> p) {
   using C = SCfg<T, L>;
   using P = typename C::P;
@@ -252,6 +255,17 @@ __global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 3 : 1)
             o[v] = fma2(oh, wh[v + q], o[v]);
           }
         }
+        // fast path: every output row of the item lies in the run and the image, pair stores
+        const int t_lo = 2 * sb, t_hi = 2 * (sb + VC);  // [t_lo, t_hi)
+        if (vec_ok && sb >= s_first && sb + VC - 1 <= s_last && t_lo >= tr0 && t_hi <= tr1 && t_lo - p.o0 >= 0 &&
+            t_hi - p.o0 <= p.N0) {
+          T *op = out + (long long)(t_lo - p.o0) * p.out_pitch + oc;
+#pragma unroll
+          for (int v = 0; v < VC; v++) {
+            *reinterpret_cast<P *>(op + (2 * v) * p.out_pitch) = e[v];
+            *reinterpret_cast<P *>(op + (2 * v + 1) * p.out_pitch) = o[v];
+          }
+        } else {
 #pragma unroll
         for (int v = 0; v < VC; v++) {
           const int s = sb + v;
@@ -270,6 +284,7 @@ __global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 3 : 1)
               if (oc + 1 >= 0 && oc + 1 < p.N1) op[1] = val.y;
             }
           }
+        }
         }
       }
       __syncthreads();  // (3) V history readers done
