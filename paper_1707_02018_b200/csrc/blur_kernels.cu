@@ -65,7 +65,10 @@ struct BCfg {
   // output columns per strip: the residual frame NH1 = TW + 2HB is a multiple of the 16-item warps
   static constexpr int TW = sizeof(T) == 4 ? (RESID ? 112 : 128) : (RESID ? 48 : 64);
   // extended rows per iteration; G >= 2HW keeps the history move [G, G+2HW) -> [0, 2HW) non-overlapping
-  static constexpr int G = (2 * HW > 16) ? 32 : 16;
+#ifndef WL_BLUR_G
+#define WL_BLUR_G 16
+#endif
+  static constexpr int G = (2 * HW > WL_BLUR_G) ? 32 : WL_BLUR_G;
   static constexpr int V = 8;                               // outputs per item, horizontal passes
   static constexpr int VC = 4;                              // output rows per item, vertical passes
   static constexpr int HB = RESID ? round_up_c(HW, 4) : 0;  // r columns beyond the tile per side
@@ -222,7 +225,7 @@ __device__ __forceinline__ void store_pair(T *row, int col, typename Pair<T>::t 
 #endif
 
 template <typename T, int HW, bool RESID>
-__global__ void __launch_bounds__(BCfg<T, HW, RESID>::NT, (sizeof(T) == 4 && BCfg<T, HW, RESID>::NT <= 256) ? WL_BLUR_MINB : 1)
+__global__ void __launch_bounds__(BCfg<T, HW, RESID>::NT, sizeof(T) == 4 ? (BCfg<T, HW, RESID>::NT <= 256 ? WL_BLUR_MINB : 2) : 1)
     k_blur_stream(const __grid_constant__ BlurStreamParams<T, HW> p) {
   using C = BCfg<T, HW, RESID>;
   using P = typename C::P;
