@@ -76,10 +76,14 @@ struct ACfg {
   static constexpr int ITEMS_B = SEGB * GI;
   static constexpr int ITEMS_C = 2 * (TQ / 2) * (G / VC);
   static constexpr int NT = round_up_c(std::max(ITEMS_B, ITEMS_C), 32);
-  static constexpr size_t OFF_U = 0;  // [2][GI][UP]
-  static constexpr size_t OFF_H = OFF_U + round_up_c(2 * GI * UP * (int)sizeof(T), 128);  // [2 sets][HR][HP]
+#ifndef WL_ANA_NS
+#define WL_ANA_NS 2  // A/B on B200: 3 or 4 stages did not beat 2
+#endif
+  static constexpr int NS = WL_ANA_NS;                   // input stages (prefetch depth NS-1)
+  static constexpr size_t OFF_U = 0;  // [NS][GI][UP]
+  static constexpr size_t OFF_H = OFF_U + round_up_c(NS * GI * UP * (int)sizeof(T), 128);  // [2 sets][HR][HP]
   static constexpr size_t OFF_BAR = OFF_H + 2 * (size_t)HR * HP * sizeof(T);
-  static constexpr size_t smem_bytes() { return OFF_BAR + 2 * sizeof(uint64_t); }
+  static constexpr size_t smem_bytes() { return OFF_BAR + NS * sizeof(uint64_t); }
 };
 
 template <typename T, int L>
@@ -107,14 +111,13 @@ __global__ void __launch_bounds__(ACfg<T, L>::NT, sizeof(T) == 4 ? 768 / ACfg<T,
   using Vt = typename Vec16<T>::type;
   constexpr int G = C::G, GI = C::GI, VEC = C::VEC, V = C::V, VC = C::VC, TQ = C::TQ;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  T *ubuf = reinterpret_cast<T *>(smem_raw + C::OFF_U);  // [2][GI][UP] input rows
+  T *ubuf = reinterpret_cast<T *>(smem_raw + C::OFF_U);  // [NS][GI][UP] input rows
   T *hist = reinterpret_cast<T *>(smem_raw + C::OFF_H);  // [2][HR][HP] lo / hi coefficient columns
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + C::OFF_BAR);
 
   const int tid = threadIdx.x;
   if (tid == 0) {
-    mbar_init(bar, 1);
-    mbar_init(bar + 1, 1);
+    for (int i = 0; i < C::NS; i++) mbar_init(bar + i, 1);
   }
   __syncthreads();
   pdl_launch_dependents();
@@ -142,16 +145,17 @@ __global__ void __launch_bounds__(ACfg<T, L>::NT, sizeof(T) == 4 ? 768 / ACfg<T,
     T *oX1 = p.out[setC + 2] + (long long)img * p.out_bstride[setC + 2];  // X = hi: HL or HH
     const long long pX0 = p.out_pitch[setC], pX1 = p.out_pitch[setC + 2];
 
-    // input block b (b = -1 .. nblk-1): rows 2(kr0 + bG) .. +2G -> ubuf[b & 1]
+    // input block b (b = -1 .. nblk-1): rows 2(kr0 + bG) .. +2G -> ubuf[(b + 1) % NS]
     auto load_block = [&](int b) -> bool {
       const int r_in = 2 * (kr0 + b * G);
-      T *dst0 = ubuf + (b & 1) * GI * C::UP;
+      const int sl = (b + 1) % C::NS;
+      T *dst0 = ubuf + sl * GI * C::UP;
       const bool inside = r_in >= 0 && r_in + GI <= p.n0 && cbox >= 0 && cbox + C::UW <= p.n1;
       if (p.tma && (p.tma_any_block || inside)) {
         if (tid == 0) {
           fence_proxy_async();
-          mbar_arrive_expect_tx(bar + (b & 1), GI * C::UW * sizeof(T));
-          tma_load_3d(dst0, &p.tmap, bar + (b & 1), cbox, r_in, img);
+          mbar_arrive_expect_tx(bar + sl, GI * C::UW * sizeof(T));
+          tma_load_3d(dst0, &p.tmap, bar + sl, cbox, r_in, img);
         }
         return true;
       }
@@ -183,17 +187,25 @@ __global__ void __launch_bounds__(ACfg<T, L>::NT, sizeof(T) == 4 ? 768 / ACfg<T,
     };
 
     __syncthreads();  // previous run's readers are done
-    bool armed = load_block(-1);
-    cp_async_commit();
+    unsigned armed = 0;  // bit s: the batch in slot s armed its barrier
+#pragma unroll
+    for (int b = -1; b < C::NS - 2; b++) {
+      if (b < nblk && load_block(b)) armed |= 1u << ((b + 1) % C::NS);
+      cp_async_commit();
+    }
     for (int it = -1; it < nblk; it++) {
-      const int slot = it & 1;
-      cp_async_wait_all();
-      if (armed) {
+      const int slot = (it + 1) % C::NS;
+      cp_async_wait_group<C::NS - 2>();  // this thread's gathers of block it are done
+      if ((armed >> slot) & 1) {
         mbar_wait(bar + slot, (phase >> slot) & 1);
         phase ^= 1u << slot;
       }
       __syncthreads();  // (1) block it landed; the history move of it-1 is done
-      armed = (it + 1 < nblk) ? load_block(it + 1) : false;
+      {
+        const int nb = it + C::NS - 1;  // its slot held block it-1, consumed before (1)
+        armed &= ~(1u << (nb + 1) % C::NS);
+        if (nb < nblk && load_block(nb)) armed |= 1u << ((nb + 1) % C::NS);
+      }
       cp_async_commit();
       // B: input row rowB of the block -> lo/hi history row L-2+rowB, coefficient columns V*segB ..
       if (actB) {

@@ -47,6 +47,8 @@ __device__ __forceinline__ void cp_async16(void *smem_dst, const void *gmem_src)
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+template <int N>  // wait until at most N committed cp.async groups are still pending
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 // Smallest pitch (elements) >= n whose size in 4-byte words is 4 mod 8: 8 rows read with
 // 16-byte loads at the same column then hit 8 distinct 4-bank groups (conflict-free).

@@ -61,10 +61,14 @@ struct SCfg {
   static constexpr int NT = round_up_c(std::max(ITEMS1, ITEMS0), 32);
   static constexpr int NCH = KCW / VEC;                  // 16-byte chunks per coefficient row
   static constexpr size_t BAND_ELEMS = (size_t)G * KCP;  // one subband window
-  static constexpr size_t OFF_C = 0;                     // [2][4][G][KCP]
-  static constexpr size_t OFF_V = OFF_C + round_up_c(2 * 4 * G * KCP * (int)sizeof(T), 128);
+#ifndef WL_SYN_NS
+#define WL_SYN_NS 2  // A/B on B200: 3 or 4 stages did not beat 2
+#endif
+  static constexpr int NS = WL_SYN_NS;                   // coefficient stages (prefetch depth NS-1)
+  static constexpr size_t OFF_C = 0;                     // [NS][4][G][KCP]
+  static constexpr size_t OFF_V = OFF_C + round_up_c(NS * 4 * G * KCP * (int)sizeof(T), 128);
   static constexpr size_t OFF_BAR = OFF_V + 2 * (size_t)HR * TWP * sizeof(T);  // VL, VH histories
-  static constexpr size_t smem_bytes() { return OFF_BAR + 2 * sizeof(uint64_t); }
+  static constexpr size_t smem_bytes() { return OFF_BAR + NS * sizeof(uint64_t); }
 };
 
 template <typename T, int L>
@@ -93,15 +97,14 @@ __global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 768 / SCfg<T,
   using Vt = typename Vec16<T>::type;
   constexpr int G = C::G, H = C::H, VEC = C::VEC, VC = C::VC, SP = C::SP;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  T *cbuf = reinterpret_cast<T *>(smem_raw + C::OFF_C);  // [2][4][G][KCP] coefficient windows
+  T *cbuf = reinterpret_cast<T *>(smem_raw + C::OFF_C);  // [NS][4][G][KCP] coefficient windows
   T *vl = reinterpret_cast<T *>(smem_raw + C::OFF_V);    // [HR][TWP] VL history (rows s)
   T *vh = vl + C::HR * C::TWP;                           // [HR][TWP] VH history
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + C::OFF_BAR);
 
   const int tid = threadIdx.x;
   if (tid == 0) {
-    mbar_init(bar, 1);
-    mbar_init(bar + 1, 1);
+    for (int i = 0; i < C::NS; i++) mbar_init(bar + i, 1);
   }
   __syncthreads();
   pdl_launch_dependents();
@@ -131,16 +134,17 @@ __global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 768 / SCfg<T,
     const bool col_in = oc + 1 >= 0 && oc < p.N1;
     const bool vec_ok = p.vec_store && oc >= 0 && oc + 1 < p.N1;
 
-    // batch k: coefficient rows s_first + kG .. of the 4 subbands -> cbuf[k & 1]
+    // batch k: coefficient rows s_first + kG .. of the 4 subbands -> cbuf[k % NS]
     auto load_batch = [&](int k) -> bool {
       const int kr = s_first + k * G;
-      T *dst0 = cbuf + (k & 1) * 4 * C::BAND_ELEMS;
+      const int sl = k % C::NS;
+      T *dst0 = cbuf + sl * 4 * C::BAND_ELEMS;
       if (p.tma) {
         if (tid == 0) {
           fence_proxy_async();
-          mbar_arrive_expect_tx(bar + (k & 1), 4 * C::BAND_ELEMS * sizeof(T));
+          mbar_arrive_expect_tx(bar + sl, 4 * C::BAND_ELEMS * sizeof(T));
 #pragma unroll
-          for (int bnd = 0; bnd < 4; bnd++) tma_load_3d(dst0 + bnd * C::BAND_ELEMS, &p.tmap[bnd], bar + (k & 1), kc0, kr, img);
+          for (int bnd = 0; bnd < 4; bnd++) tma_load_3d(dst0 + bnd * C::BAND_ELEMS, &p.tmap[bnd], bar + sl, kc0, kr, img);
         }
         return true;
       }
@@ -181,20 +185,29 @@ __global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 768 / SCfg<T,
     };
 
     __syncthreads();  // previous run's readers are done
-    bool armed = load_batch(0);
-    cp_async_commit();
+    unsigned armed = 0;  // bit s: the batch in slot s armed its barrier
+#pragma unroll
+    for (int k = 0; k < C::NS - 1; k++) {
+      if (k < n_it && load_batch(k)) armed |= 1u << (k % C::NS);
+      cp_async_commit();
+    }
     for (int it = 0; it < n_it; it++) {
-      cp_async_wait_all();
-      if (armed) {
-        mbar_wait(bar + (it & 1), (phase >> (it & 1)) & 1);
-        phase ^= 1u << (it & 1);
+      const int slot = it % C::NS;
+      cp_async_wait_group<C::NS - 2>();  // this thread's gathers of batch it are done
+      if ((armed >> slot) & 1) {
+        mbar_wait(bar + slot, (phase >> slot) & 1);
+        phase ^= 1u << slot;
       }
       __syncthreads();  // (1) batch it landed; the history move of it-1 is done
-      armed = (it + 1 < n_it) ? load_batch(it + 1) : false;
+      {
+        const int nb = it + C::NS - 1;  // its slot held batch it-1, consumed before (1)
+        armed &= ~(1u << (nb % C::NS));
+        if (nb < n_it && load_batch(nb)) armed |= 1u << (nb % C::NS);
+      }
       cp_async_commit();
       // S1: coefficient row r of the batch -> V rows (history index H-1+r), output pairs SP*seg1 ..
       if (act1) {
-        const T *cb = cbuf + (it & 1) * 4 * C::BAND_ELEMS + row1 * C::KCP + SP * seg1;
+        const T *cb = cbuf + (it % C::NS) * 4 * C::BAND_ELEMS + row1 * C::KCP + SP * seg1;
 #pragma unroll 1
         for (int pr = 0; pr < 2; pr++) {  // pr 0: (LL, LH) -> VL; 1: (HL, HH) -> VH
           T a[C::NWC], d[C::NWC];
