@@ -36,6 +36,7 @@
 #define WLO_FOLD_CROP 0     /* y[i] = u[i], i in [0, n)               */
 #define WLO_FOLD_WRAP 1     /* y[i] = sum_{t = i mod n} u[t]          */
 #define WLO_FOLD_SYM_PINV 2 /* y = E_sym^dagger u = diag(1/c) E_sym^T u */
+#define WLO_FOLD_SYM_T 3    /* y = E_sym^T u  (reflect-add; the adjoint of W-dagger's E_sym) */
 
 /* ---------------------------------------------------------------- extension */
 
@@ -248,12 +249,14 @@ int wlo_analysis2d(const double *img, long B, long h, long w, int J, const doubl
 
 /* Multi-level 2-D synthesis (the transpose of wlo_analysis2d with the same filters
  * and the fold that is the adjoint of its extension: CROP <-> ZERO, WRAP <-> PER,
- * SYM_PINV <-> SYM_PADJ).  x: [B, p] packed; img: [B, h, w]. */
+ * SYM_PINV <-> SYM_PADJ, SYM_T <-> SYM).  x: [B, p] packed; img: [B, h, w]. */
 int wlo_synthesis2d(const double *x, long B, long h, long w, int J, const double *glo,
                     const double *ghi, int L, int fold, double *img) {
   long c0[40], c1[40];
-  int chain_kind = fold == WLO_FOLD_WRAP ? WLO_EXT_PER
-                   : fold == WLO_FOLD_SYM_PINV ? WLO_EXT_SYM_PADJ : WLO_EXT_ZERO;
+  int chain_kind = fold == WLO_FOLD_WRAP       ? WLO_EXT_PER
+                   : fold == WLO_FOLD_SYM_PINV ? WLO_EXT_SYM_PADJ
+                   : fold == WLO_FOLD_SYM_T    ? WLO_EXT_SYM
+                                               : WLO_EXT_ZERO;
   if (J < 1 || J > 32) return 1;
   if (wlo_chain(h, L, chain_kind, J, c0) != 0 || wlo_chain(w, L, chain_kind, J, c1) != 0) return 2;
   long p = packed_size(c0, c1, J);

@@ -10,6 +10,7 @@ Operators (PAPER.md §"Example 1: An Image Deblurring Problem"):
   analyze    W-dagger = W-dagger_zpd E_bc
   adjoint    W*       = W~dagger_zpd (E^dagger)*                    (Eq. (4))
   synthesize W        = (W*)^T                                      (reading R1)
+  analyze_adjoint (W-dagger)* = E_bc^T A_a^T
   blur       R        (Gaussian PSF, symmetric BC)
   blur_adjoint R*
   grad       grad f(x) = W* R* (R W x - b),  f = 1/2 ||R W x - b||^2
@@ -32,7 +33,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
 EXT_ZERO, EXT_PER, EXT_SYM, EXT_SYM_PADJ = 0, 1, 2, 3
-FOLD_CROP, FOLD_WRAP, FOLD_SYM_PINV = 0, 1, 2
+FOLD_CROP, FOLD_WRAP, FOLD_SYM_PINV, FOLD_SYM_T = 0, 1, 2, 3
 
 BCS = ("zero", "periodic", "symmetric", "symmetric_edag")
 
@@ -194,6 +195,15 @@ def synthesize(x, h: int, w: int, J: int, filt: str, bc: str) -> np.ndarray:
     fb = filter_bank(filt)
     fold = {"zero": FOLD_CROP, "periodic": FOLD_WRAP, "symmetric": FOLD_CROP, "symmetric_edag": FOLD_SYM_PINV}[bc]
     return _synthesis(x, h, w, J, fb.d_lo, fb.d_hi, fb.L, fold)
+
+
+def analyze_adjoint(x, h: int, w: int, J: int, filt: str, bc: str) -> np.ndarray:
+    """(W-dagger)*: the adjoint of the analysis W-dagger = A_a E_bc (P:47 "(and analysis)";
+    SURVEY §8(f) NEXT #2): scatter with the ANALYSIS filters, then fold with E_bc^T --
+    truncate (zero), wrap-add (periodic), reflect-add (symmetric, symmetric_edag)."""
+    fb = filter_bank(filt)
+    fold = {"zero": FOLD_CROP, "periodic": FOLD_WRAP, "symmetric": FOLD_SYM_T, "symmetric_edag": FOLD_SYM_T}[bc]
+    return _synthesis(x, h, w, J, fb.a_lo, fb.a_hi, fb.L, fold)
 
 
 def blur(img, taps=None) -> np.ndarray:

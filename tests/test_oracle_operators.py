@@ -229,3 +229,44 @@ def test_grad(oracle_lib, filt, bc):
     b0 = (R @ (Wm @ x)).reshape(h, w)
     g0, f0 = O.grad(x, b0, J, filt, bc)
     assert np.abs(g0).max() < 1e-13 and f0 < 1e-26
+
+
+# ------------------------------------------------ (W-dagger)*: SURVEY §8(f) NEXT #2
+@pytest.mark.parametrize("filt", FILTERS)
+@pytest.mark.parametrize("bc", BCS)
+def test_analyze_adjoint_is_dense_transpose(oracle_lib, filt, bc):
+    """(W-dagger)* (scatter loops with the analysis filters + E_bc^T fold) equals the transpose of
+    W-dagger assembled column by column from the analysis loops; adjoint identity."""
+    O = oracle_lib
+    h, w, J = _shape(bc, filt)
+    A = dense_Wdag(O, h, w, J, filt, bc)                                         # (p, hw)
+    p = A.shape[0]
+    At = O.analyze_adjoint(np.eye(p), h, w, J, filt, bc).reshape(p, h * w).T     # (hw, p)
+    assert np.abs(A.T - At).max() <= 1e-15 * max(1.0, np.abs(A).max()) * 8
+    rng = np.random.default_rng(17)
+    x = rng.standard_normal(p)
+    y = rng.standard_normal((h, w))
+    lhs = np.vdot(O.analyze(y, J, filt, bc), x)
+    rhs = np.vdot(y, O.analyze_adjoint(x, h, w, J, filt, bc))
+    assert abs(lhs - rhs) <= 1e-13 * np.linalg.norm(x) * np.linalg.norm(y)
+
+
+@pytest.mark.parametrize("filt", [f for f in FILTERS if filter_bank(f).orthogonal])
+def test_analyze_adjoint_orthogonal_periodic_is_W(oracle_lib, filt):
+    """Orthogonal + periodic: W-dagger = W* = W^{-1} (BJ north_star), so (W-dagger)* = W."""
+    O = oracle_lib
+    h, w, J = 16, 24, 2
+    x = np.random.default_rng(3).standard_normal(O.layout(h, w, J, filt, "periodic").p)
+    np.testing.assert_allclose(O.analyze_adjoint(x, h, w, J, filt, "periodic"),
+                               O.synthesize(x, h, w, J, filt, "periodic"), rtol=0, atol=1e-13)
+
+
+def test_analyze_adjoint_symmetric_differs_from_W(oracle_lib):
+    """Under symmetric BC, (W-dagger)* folds reflect-add with the analysis filters, so for CDF 9/7
+    it differs from W (crop, dual filters) by far more than rounding: a guard against swapping them."""
+    O = oracle_lib
+    h, w, J = 24, 20, 2
+    x = np.random.default_rng(4).standard_normal(O.layout(h, w, J, "cdf97", "symmetric").p)
+    a = O.analyze_adjoint(x, h, w, J, "cdf97", "symmetric")
+    b = O.synthesize(x, h, w, J, "cdf97", "symmetric")
+    assert np.linalg.norm(a - b) > 0.05 * np.linalg.norm(b)
