@@ -94,7 +94,13 @@ typedef enum {
 
 typedef enum { WL_F32 = 0, WL_F64 = 1 } wl_dtype;
 
-typedef enum { WL_OP_SYNTHESIZE = 0, WL_OP_ADJOINT = 1, WL_OP_ANALYZE = 2, WL_OP_GRAD = 3 } wl_op;
+typedef enum {
+  WL_OP_SYNTHESIZE = 0,
+  WL_OP_ADJOINT = 1,
+  WL_OP_ANALYZE = 2,
+  WL_OP_GRAD = 3,
+  WL_OP_ANALYZE_ADJOINT = 4
+} wl_op;
 
 typedef struct wl_plan wl_plan;           /* opaque, immutable after create */
 typedef struct wl_blur_plan wl_blur_plan; /* opaque, immutable after create */
@@ -150,6 +156,13 @@ WL_API wl_status wl_adjoint(const wl_plan *plan, int64_t batch, const void *img,
  * filters after the boundary extension E_bc.  W W-dagger = I except for SYMMETRIC_EDAG. */
 WL_API wl_status wl_analyze(const wl_plan *plan, int64_t batch, const void *img, void *x, void *ws,
                      void *stream);
+/* (W-dagger)* (the adjoint "(and analysis)"): coefficients
+ * x [batch, p_alloc] -> images img [batch, h, w], the exact transpose of wl_analyze:
+ * upsample-convolve with the ANALYSIS filters, then fold with E_bc^T -- truncate (zero),
+ * wrap-add (periodic), unweighted reflect-add (symmetric, symmetric_edag).
+ * ws: wl_workspace_bytes(plan, NULL, WL_OP_ANALYZE_ADJOINT, batch). */
+WL_API wl_status wl_analyze_adjoint(const wl_plan *plan, int64_t batch, const void *x, void *img, void *ws,
+                             void *stream);
 
 /* ------------------------------------------------------------------- blur */
 

@@ -95,7 +95,8 @@ WsLayout ws_layout(const wl_plan *p, const wl_blur_plan *bl, wl_op op, int64_t b
   L.a = off; off = align256(off + B * (size_t)p->ws_a_elems * es);
   L.b = off; off = align256(off + B * (size_t)p->ws_b_elems * es);
   L.e = off;
-  if ((op == WL_OP_SYNTHESIZE || op == WL_OP_GRAD) && p->bc == WL_BC_SYMMETRIC_EDAG)
+  if (((op == WL_OP_SYNTHESIZE || op == WL_OP_GRAD) && p->bc == WL_BC_SYMMETRIC_EDAG) ||
+      (op == WL_OP_ANALYZE_ADJOINT && (p->bc == WL_BC_SYMMETRIC_EDAG || p->bc == WL_BC_SYMMETRIC)))
     off = align256(off + B * (size_t)p->edag_elems * es);
   L.u = off;
   L.s = off;
@@ -178,9 +179,13 @@ wl_status run_analysis(const wl_plan *p, int64_t batch, const void *img, void *x
 }
 
 // synthesis chain (W) ------------------------------------------------------------
+// Multi-level upsample-convolve chain, coarse -> fine.  transpose_of_analysis = false: W
+// (dual filters; crop / periodic / weighted EDAG fold); true: (W-dagger)* (analysis filters;
+// crop / periodic / unweighted reflect-add fold, the adjoint of W-dagger's E_bc).
 wl_status run_synthesis(const wl_plan *p, int64_t batch, const void *x, void *img, char *ws, const WsLayout &L,
-                        cudaStream_t s) {
+                        cudaStream_t s, bool transpose_of_analysis = false) {
   const int Lp = p->fb.L - 1;
+  const bool sym = p->bc == WL_BC_SYMMETRIC_EDAG || (transpose_of_analysis && p->bc == WL_BC_SYMMETRIC);
   for (int j = p->J; j >= 1; j--) {
     SynthesisArgs a;
     Buf ll = (j == p->J) ? band_buf(p, x, 0) : ll_buf(p, ws, L, j);
@@ -194,8 +199,8 @@ wl_status run_synthesis(const wl_plan *p, int64_t batch, const void *x, void *im
     a.m0 = (int)p->n0[j];
     a.m1 = (int)p->n1[j];
     a.coef_mod = p->bc == WL_BC_PERIODIC;
-    a.lo = p->fb.d_lo;
-    a.hi = p->fb.d_hi;
+    a.lo = transpose_of_analysis ? p->fb.a_lo : p->fb.d_lo;
+    a.hi = transpose_of_analysis ? p->fb.a_hi : p->fb.d_hi;
     a.L = p->fb.L;
     a.batch = (int)batch;
     int64_t n0 = p->n0[j - 1], n1 = p->n1[j - 1];
@@ -207,8 +212,9 @@ wl_status run_synthesis(const wl_plan *p, int64_t batch, const void *x, void *im
     } else {
       out = ll_buf(p, ws, L, j - 1);
     }
-    if (p->bc == WL_BC_SYMMETRIC_EDAG) {
-      // W_P = E_sym^dagger W_zpd: synthesize onto [-L', n+L') per axis, then weighted fold
+    if (sym) {
+      // synthesize onto [-L', n+L') per axis, then fold: E_sym^dagger (W of EDAG) or
+      // E_sym^T ((W-dagger)* under symmetric BC)
       int64_t ep = round_up(n1 + 2 * Lp, 16 / p->es);
       a.out = ws + L.e;
       a.out_pitch = ep;
@@ -229,6 +235,7 @@ wl_status run_synthesis(const wl_plan *p, int64_t batch, const void *x, void *im
       f.n0 = (int)n0;
       f.n1 = (int)n1;
       f.Lp = Lp;
+      f.weighted = transpose_of_analysis ? 0 : 1;
       f.batch = (int)batch;
       e = launch_fold(p->dtype, f, s);
       if (e != cudaSuccess) return cuda_fail(e, "fold launch");
@@ -343,7 +350,7 @@ wl_status wl_plan_create(wl_plan **out, int64_t h, int64_t w, int levels, wl_fil
     if (j % 2) p->ws_a_elems = std::max(p->ws_a_elems, e);
     else p->ws_b_elems = std::max(p->ws_b_elems, e);
   }
-  if (bc == WL_BC_SYMMETRIC_EDAG)
+  if (bc == WL_BC_SYMMETRIC_EDAG || bc == WL_BC_SYMMETRIC)  // extended synthesis buffer (W of EDAG, (W-dagger)*)
     for (int j = 1; j <= levels; j++)
       p->edag_elems = std::max(p->edag_elems, (p->n0[j - 1] + 2 * (L - 1)) * round_up(p->n1[j - 1] + 2 * (L - 1), align));
   *out = p;
@@ -419,6 +426,21 @@ wl_status wl_synthesize(const wl_plan *p, int64_t batch, const void *x, void *im
   if (L.total && (overlap(ws, L.total, img, ib) || overlap(ws, L.total, x, xb)))
     return fail(WL_EINVAL, "wl_synthesize: ws overlaps img or x");
   st = run_synthesis(p, batch, x, img, (char *)ws, L, (cudaStream_t)stream);
+  return st ? st : ok();
+}
+
+wl_status wl_analyze_adjoint(const wl_plan *p, int64_t batch, const void *x, void *img, void *ws, void *stream) {
+  if (check_plan(p)) return WL_EINVAL;
+  if (batch < 0) return fail(WL_EINVAL, "wl_analyze_adjoint: batch=%lld < 0", (long long)batch);
+  if (batch == 0) return ok();
+  size_t ib = (size_t)batch * p->h * p->w * p->es, xb = (size_t)batch * p->p_alloc * p->es;
+  wl_status st = check_io(x, xb, "x", img, ib, "img");
+  if (st) return st;
+  if ((st = check_ws(p, nullptr, WL_OP_ANALYZE_ADJOINT, batch, ws))) return st;
+  WsLayout L = ws_layout(p, nullptr, WL_OP_ANALYZE_ADJOINT, batch);
+  if (L.total && (overlap(ws, L.total, img, ib) || overlap(ws, L.total, x, xb)))
+    return fail(WL_EINVAL, "wl_analyze_adjoint: ws overlaps img or x");
+  st = run_synthesis(p, batch, x, img, (char *)ws, L, (cudaStream_t)stream, true);
   return st ? st : ok();
 }
 

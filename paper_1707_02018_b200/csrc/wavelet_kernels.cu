@@ -1,6 +1,8 @@
-// The weighted fold of the paper-literal symmetric variant (SYMMETRIC_EDAG, reading R1):
-// W = E_sym^dagger W_zpd, i.e. y = diag(1/c) E_sym^T U per axis after the synthesis kernel
-// (synthesis_kernels.cu) has written U over the extended range [-L', n+L').
+// The symmetric folds after a synthesis onto the extended range [-L', n+L') per axis
+// (synthesis_kernels.cu writes U there):
+//   weighted   W of the paper-literal variant (SYMMETRIC_EDAG, reading R1): y = E_sym^dagger U
+//              = diag(1/c) E_sym^T U;
+//   unweighted (W-dagger)* under symmetric BC: y = E_sym^T U (reflect-add).
 // Analysis (W*, W-dagger) lives in analysis_kernels.cu.
 #include <cuda_runtime.h>
 
@@ -15,7 +17,7 @@ namespace {
 // ------------------------------------------------------------- EDAG fold
 template <typename T>
 __global__ void k_fold_sym_pinv(const T *__restrict__ U, long long upitch, long long ubs, T *__restrict__ y,
-                                long long ypitch, long long ybs, int n0, int n1, int Lp) {
+                                long long ypitch, long long ybs, int n0, int n1, int Lp, int weighted) {
   int pcol = blockIdx.x * blockDim.x + threadIdx.x;
   int i = blockIdx.y;
   int b = blockIdx.z;
@@ -31,7 +33,7 @@ __global__ void k_fold_sym_pinv(const T *__restrict__ U, long long upitch, long 
   T acc = T(0);
   for (int a = 0; a < c0; a++)
     for (int c = 0; c < c1; c++) acc += u[(long long)(t0s[a] + Lp) * upitch + (t1s[c] + Lp)];
-  y[(long long)b * ybs + (long long)i * ypitch + pcol] = acc / T(c0 * c1);
+  y[(long long)b * ybs + (long long)i * ypitch + pcol] = weighted ? acc / T(c0 * c1) : acc;
 }
 
 }  // namespace
@@ -42,11 +44,11 @@ cudaError_t launch_fold(int dtype, const FoldArgs &a, cudaStream_t s) {
   if (dtype == WL_F64)
     k_fold_sym_pinv<double><<<grid, 128, 0, s>>>(static_cast<const double *>(a.in), a.in_pitch, a.in_bstride,
                                                  static_cast<double *>(a.out), a.out_pitch, a.out_bstride, a.n0,
-                                                 a.n1, a.Lp);
+                                                 a.n1, a.Lp, a.weighted);
   else
     k_fold_sym_pinv<float><<<grid, 128, 0, s>>>(static_cast<const float *>(a.in), a.in_pitch, a.in_bstride,
                                                static_cast<float *>(a.out), a.out_pitch, a.out_bstride, a.n0,
-                                               a.n1, a.Lp);
+                                               a.n1, a.Lp, a.weighted);
   g_launches++;
   return cudaGetLastError();
 }

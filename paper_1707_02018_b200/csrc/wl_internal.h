@@ -52,12 +52,13 @@ struct SynthesisArgs {
   int batch;
 };
 
-struct FoldArgs {  // y = diag(1/c) E_sym^T U per axis (W of the SYMMETRIC_EDAG variant)
+struct FoldArgs {  // y = diag(1/c) E_sym^T U per axis (weighted: W of SYMMETRIC_EDAG) or E_sym^T U
   const void *in;
   int64_t in_pitch, in_bstride;  // U over [-Lp, n+Lp) per axis
   void *out;
   int64_t out_pitch, out_bstride;
   int n0, n1, Lp;
+  int weighted;                  // 1: E_sym^dagger = diag(1/c) E_sym^T; 0: E_sym^T ((W-dagger)*)
   int batch;
 };
 

@@ -23,7 +23,7 @@ _LIB_PATH = os.environ.get("WL_LIB") or os.path.join(_PKG, "libwl.so")   # WL_LI
 WL_OK, WL_EINVAL, WL_ESIZE, WL_EDTYPE, WL_EALIGN, WL_ENOMEM, WL_ECUDA = range(7)
 FILTERS = {"haar": 1, "db1": 1, "db2": 2, "db4": 4, "db8": 8, "cdf97": 97}
 BCS = {"zero": 0, "periodic": 1, "symmetric": 2, "symmetric_edag": 3}
-OP_SYNTHESIZE, OP_ADJOINT, OP_ANALYZE, OP_GRAD = range(4)
+OP_SYNTHESIZE, OP_ADJOINT, OP_ANALYZE, OP_GRAD, OP_ANALYZE_ADJOINT = range(5)
 MAX_LEVELS = 32
 
 
@@ -45,7 +45,7 @@ class _PlanInfo(ctypes.Structure):
 
 
 EXPORTS = ("wl_plan_create", "wl_plan_destroy", "wl_plan_query", "wl_plan_filters", "wl_workspace_bytes",
-           "wl_synthesize", "wl_adjoint", "wl_analyze", "wl_blur_create", "wl_blur_create_gaussian",
+           "wl_synthesize", "wl_adjoint", "wl_analyze", "wl_analyze_adjoint", "wl_blur_create", "wl_blur_create_gaussian",
            "wl_blur_destroy", "wl_blur_taps", "wl_blur", "wl_blur_adjoint", "wl_blur_residual_adjoint",
            "wl_grad", "wl_last_error", "wl_launch_count", "wl_version")
 
@@ -73,7 +73,7 @@ def lib():
     L.wl_plan_filters.argtypes = [vp, dp, dp, dp, dp]
     L.wl_workspace_bytes.argtypes = [vp, vp, ci, i64]
     L.wl_workspace_bytes.restype = ctypes.c_size_t
-    for fn in ("wl_synthesize", "wl_adjoint", "wl_analyze"):
+    for fn in ("wl_synthesize", "wl_adjoint", "wl_analyze", "wl_analyze_adjoint"):
         getattr(L, fn).argtypes = [vp, i64, vp, vp, vp, vp]
     L.wl_blur_create.argtypes = [ctypes.POINTER(vp), i64, i64, dp, ci, ci, ci]
     L.wl_blur_create_gaussian.argtypes = [ctypes.POINTER(vp), i64, i64, ci, cd, ci, ci]
@@ -205,17 +205,24 @@ class Plan:
     def _batch_of(self, t, trailing):
         return int(np.prod(t.shape[:-trailing])) if t.dim() > trailing else 1
 
-    def synthesize(self, x, out=None, ws=None, stream=None):
-        """W: x [..., p_alloc] -> image [..., h, w]."""
+    def _synthesis(self, fn, op, x, out, ws, stream):
         torch = _torch()
         _require(x, "x", self.torch_dtype, (self.p_alloc,))
         B = self._batch_of(x, 1)
         if out is None:
             out = torch.empty(x.shape[:-1] + (self.h, self.w), dtype=x.dtype, device=x.device)
         _require(out, "img", self.torch_dtype, (self.h, self.w))
-        ws = self._ws(OP_SYNTHESIZE, B, ws=ws)
-        _check(lib().wl_synthesize(self._h, B, _ptr(x), _ptr(out), _ptr(ws), _stream_ptr(stream)))
+        ws = self._ws(op, B, ws=ws)
+        _check(fn(self._h, B, _ptr(x), _ptr(out), _ptr(ws), _stream_ptr(stream)))
         return out
+
+    def synthesize(self, x, out=None, ws=None, stream=None):
+        """W: x [..., p_alloc] -> image [..., h, w]."""
+        return self._synthesis(lib().wl_synthesize, OP_SYNTHESIZE, x, out, ws, stream)
+
+    def analyze_adjoint(self, x, out=None, ws=None, stream=None):
+        """(W-dagger)*: x [..., p_alloc] -> image [..., h, w], the transpose of analyze()."""
+        return self._synthesis(lib().wl_analyze_adjoint, OP_ANALYZE_ADJOINT, x, out, ws, stream)
 
     def _analysis(self, fn, op, img, out, ws, stream):
         torch = _torch()

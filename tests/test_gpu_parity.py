@@ -77,6 +77,13 @@ def test_operators_match_oracle(torch, filt, bc, dtype, shape):
         lhs = np.vdot(g_syn[b], y[b])
         rhs = np.vdot(xp[b], plan.to_packed(g_adj[b]))
         assert abs(lhs - rhs) / (np.linalg.norm(g_syn[b]) * np.linalg.norm(y[b])) <= ADJ[dtype]
+    # (W-dagger)*: the transpose of W-dagger (analysis filters, E_bc^T fold)
+    g_aad = host(plan.analyze_adjoint(xd))
+    assert rel(g_aad, O.analyze_adjoint(xp, h, w, J, filt, bc)) <= TOL[dtype]
+    for b in range(B):
+        lhs = np.vdot(g_aad[b], y[b])
+        rhs = np.vdot(xp[b], plan.to_packed(g_ana[b]))
+        assert abs(lhs - rhs) / (np.linalg.norm(g_aad[b]) * np.linalg.norm(y[b])) <= ADJ[dtype]
     # perfect reconstruction on the GPU (not for the paper-literal variant, which is interior-only)
     if bc != "symmetric_edag":
         rec = host(plan.synthesize(plan.analyze(yd)))
@@ -178,6 +185,8 @@ def test_config_operators_full_size(torch, cfg):
     if "Wdag" in c.ops:
         ga = host(plan.analyze(yd))
         assert rel(plan.to_packed(ga), O.analyze(y, c.levels, c.filt, c.bc)) <= TOL[c.dtype]
+        gt = host(plan.analyze_adjoint(xd))
+        assert rel(gt, O.analyze_adjoint(x, c.h, c.w, c.levels, c.filt, c.bc)) <= TOL[c.dtype]
     for b in range(c.batch):
         d = abs(np.vdot(gw[b], y[b]) - np.vdot(x[b], plan.to_packed(gs[b])))
         assert d / (np.linalg.norm(gw[b]) * np.linalg.norm(y[b])) <= ADJ[c.dtype]

@@ -2,7 +2,7 @@
 """Per-operator timing on one GPU (development tool; bench.py is the contract).
 
   python tools/opbench.py --cfg 4 --op adjoint --reps 50
-ops: adjoint, analyze, synthesize, blur, residual, grad.  Prints one JSON line per op with
+ops: adjoint, analyze, analyze_adjoint, synthesize, blur, residual, grad.  Prints one JSON line per op with
 device ms per call (CUDA events, warm L2 for small configs).
 """
 import argparse
@@ -46,6 +46,10 @@ def main():
         elif op == "analyze":
             ws = plan._ws(wl.OP_ANALYZE, B)
             fn = lambda: plan.analyze(img, out=out_x, ws=ws)  # noqa: E731
+            nbytes = (c.h * c.w + plan.p_valid) * B * plan.torch_dtype.itemsize
+        elif op == "analyze_adjoint":
+            ws = plan._ws(wl.OP_ANALYZE_ADJOINT, B)
+            fn = lambda: plan.analyze_adjoint(x, out=out_i, ws=ws)  # noqa: E731
             nbytes = (c.h * c.w + plan.p_valid) * B * plan.torch_dtype.itemsize
         elif op == "synthesize":
             ws = plan._ws(wl.OP_SYNTHESIZE, B)
