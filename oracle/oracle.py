@@ -239,3 +239,49 @@ def grad(x, b, J: int, filt: str, bc: str, taps=None):
     g = adjoint(s, J, filt, bc)
     f = 0.5 * np.sum(r.reshape(r.shape[:-2] + (-1,)) ** 2, axis=-1)
     return g, f
+
+
+# ------------------------------------------------- FISTA: SURVEY §8(f) NEXT #1
+def soft_threshold(v, tau):
+    """prox of tau ||.||_1: sign(v) max(|v| - tau, 0)."""
+    return np.sign(v) * np.maximum(np.abs(v) - tau, 0.0)
+
+
+def fista_update(g, x, y, t, lam, lip):
+    """One FISTA update (Beck & Teboulle 2009, cited at P:117) from g = grad f(y):
+        x+ = soft(y - g / L, lam / L);  t+ = (1 + sqrt(1 + 4 t^2)) / 2;  y+ = x+ + ((t - 1) / t+)(x+ - x).
+    Returns (x+, y+, t+)."""
+    x_new = soft_threshold(y - g / lip, lam / lip)
+    t_new = (1.0 + np.sqrt(1.0 + 4.0 * t * t)) / 2.0
+    y_new = x_new + ((t - 1.0) / t_new) * (x_new - x)
+    return x_new, y_new, t_new
+
+
+def fista(x0, b, J: int, filt: str, bc: str, lam: float, lip: float, iters: int, taps=None):
+    """FISTA on min_x 1/2 ||R W x - b||^2 + lam ||x||_1 (Eq. (1)): `iters` steps from x0,
+    y_1 = x0, t_1 = 1.  Returns (x, y, t, objective trace F(x_k))."""
+    x = np.array(x0, dtype=np.float64)
+    y = x.copy()
+    t = 1.0
+    trace = []
+    for _ in range(iters):
+        g, _f = grad(y, b, J, filt, bc, taps)
+        x, y, t = fista_update(g, x, y, t, lam, lip)
+        _g, fx = grad(x, b, J, filt, bc, taps)
+        trace.append(fx + lam * np.abs(x).reshape(x.shape[0] if x.ndim > 1 else 1, -1).sum(axis=-1))
+    return x, y, t, np.array(trace)
+
+
+def lipschitz(v0, h: int, w: int, J: int, filt: str, bc: str, iters: int, taps=None):
+    """Power iteration for L = lambda_max(W* R* R W) (the Lipschitz constant of grad f):
+    v <- G v / ||G v|| with G v = grad f(v) at b = 0; returns the Rayleigh quotient <v, G v> / <v, v>
+    of the last iterate (a lower bound of L that increases to it)."""
+    v = np.array(v0, dtype=np.float64).reshape(1, -1)
+    zero = np.zeros((1, h, w))
+    est = 0.0
+    for _ in range(iters):
+        v = v / np.linalg.norm(v)
+        gv, _f = grad(v, zero, J, filt, bc, taps)
+        est = float(np.vdot(v, gv))
+        v = gv
+    return est
