@@ -99,7 +99,9 @@ typedef enum {
   WL_OP_ADJOINT = 1,
   WL_OP_ANALYZE = 2,
   WL_OP_GRAD = 3,
-  WL_OP_ANALYZE_ADJOINT = 4
+  WL_OP_ANALYZE_ADJOINT = 4,
+  WL_OP_FISTA = 5,
+  WL_OP_LIPSCHITZ = 6
 } wl_op;
 
 typedef struct wl_plan wl_plan;           /* opaque, immutable after create */
@@ -196,6 +198,30 @@ WL_API wl_status wl_blur_residual_adjoint(const wl_blur_plan *blur, int64_t batc
  * The plans must agree in h, w and dtype.  ws: wl_workspace_bytes(plan, blur, WL_OP_GRAD, batch). */
 WL_API wl_status wl_grad(const wl_plan *plan, const wl_blur_plan *blur, int64_t batch, const void *x,
                   const void *b, void *g, double *f_dev, void *ws, void *stream);
+
+/* ------------------------------------------------------------- FISTA */
+
+/* FISTA (Beck & Teboulle 2009; the solver of P:117 and P:174, 2500 iterations there) for
+ *     min_x 1/2 ||R W x - b||^2 + lambda ||x||_1      (Eq. (1)).
+ * wl_fista_update: given g = grad f(y) [batch, p_alloc], in place
+ *     x <- soft(y - g / lip, lambda / lip),  t+ = (1 + sqrt(1 + 4 t^2)) / 2,
+ *     y <- x + ((t - 1) / t+) (x - x_old).
+ * t is the host-side momentum scalar of the current step (t_1 = 1; the caller advances it with
+ * the same formula).  lip > 0 is the Lipschitz constant of grad f (wl_lipschitz), lambda >= 0.
+ * Pitch padding stays 0.  x, y, g must not overlap (WL_EINVAL). */
+WL_API wl_status wl_fista_update(const wl_plan *plan, int64_t batch, const void *g, void *x, void *y, double t,
+                          double lambda, double lip, void *stream);
+/* One full FISTA iteration: g = grad f(y) (wl_grad; f_dev, nullable, receives f(y)), then
+ * wl_fista_update.  ws: wl_workspace_bytes(plan, blur, WL_OP_FISTA, batch). */
+WL_API wl_status wl_fista_step(const wl_plan *plan, const wl_blur_plan *blur, int64_t batch, const void *b, void *x,
+                        void *y, double t, double lambda, double lip, double *f_dev, void *ws, void *stream);
+/* Power iteration for lip = lambda_max(W* R* R W): v_0 = a seeded uniform(-1, 1)
+ * vector, v <- G v with G v = grad f(v) at b = 0, estimate <v, G v> / <v, v> of the last step
+ * (a lower bound that increases to lambda_max).  Blocking: synchronises `stream` every iteration
+ * to rescale v.  *lip_host (host pointer) receives the estimate.
+ * ws: wl_workspace_bytes(plan, blur, WL_OP_LIPSCHITZ, 1). */
+WL_API wl_status wl_lipschitz(const wl_plan *plan, const wl_blur_plan *blur, int iters, uint64_t seed,
+                       double *lip_host, void *ws, void *stream);
 
 /* ---------------------------------------------------------------- misc */
 

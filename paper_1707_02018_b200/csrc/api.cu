@@ -85,7 +85,7 @@ bool overlap(const void *a, size_t na, const void *b, size_t nb) {
 
 // workspace carve-up ---------------------------------------------------------
 struct WsLayout {
-  size_t a = 0, b = 0, e = 0, u = 0, s = 0, total = 0;  // byte offsets
+  size_t a = 0, b = 0, e = 0, u = 0, s = 0, g = 0, v = 0, b0 = 0, d = 0, total = 0;  // byte offsets
 };
 
 WsLayout ws_layout(const wl_plan *p, const wl_blur_plan *bl, wl_op op, int64_t batch) {
@@ -95,17 +95,28 @@ WsLayout ws_layout(const wl_plan *p, const wl_blur_plan *bl, wl_op op, int64_t b
   L.a = off; off = align256(off + B * (size_t)p->ws_a_elems * es);
   L.b = off; off = align256(off + B * (size_t)p->ws_b_elems * es);
   L.e = off;
-  if (((op == WL_OP_SYNTHESIZE || op == WL_OP_GRAD) && p->bc == WL_BC_SYMMETRIC_EDAG) ||
+  if (((op == WL_OP_SYNTHESIZE || op == WL_OP_GRAD || op == WL_OP_FISTA || op == WL_OP_LIPSCHITZ) &&
+       p->bc == WL_BC_SYMMETRIC_EDAG) ||
       (op == WL_OP_ANALYZE_ADJOINT && (p->bc == WL_BC_SYMMETRIC_EDAG || p->bc == WL_BC_SYMMETRIC)))
     off = align256(off + B * (size_t)p->edag_elems * es);
   L.u = off;
   L.s = off;
-  if (op == WL_OP_GRAD) {
+  if (op == WL_OP_GRAD || op == WL_OP_FISTA || op == WL_OP_LIPSCHITZ) {
     size_t img = B * (size_t)p->h * (size_t)p->w * es;
     L.u = off; off = align256(off + img);
     L.s = off; off = align256(off + img);
   }
   (void)bl;
+  if (op == WL_OP_FISTA) {  // + g = grad f(y)
+    L.g = off;
+    off = align256(off + B * (size_t)p->p_alloc * es);
+  }
+  if (op == WL_OP_LIPSCHITZ) {  // + v, g (one image), a zero image b0, two fp64 scalars
+    L.v = off; off = align256(off + (size_t)p->p_alloc * es);
+    L.g = off; off = align256(off + (size_t)p->p_alloc * es);
+    L.b0 = off; off = align256(off + (size_t)p->h * p->w * es);
+    L.d = off; off = align256(off + 2 * sizeof(double));
+  }
   L.total = off;
   return L;
 }
@@ -274,6 +285,10 @@ wl_status check_io(const void *in, size_t in_bytes, const char *in_name, const v
   if (overlap(in, in_bytes, out, out_bytes)) return fail(WL_EINVAL, "%s and %s overlap", in_name, out_name);
   return WL_OK;
 }
+
+// g = W* R* (R W x - b) into g (W chain -> fused residual -> W* chain), no validation.
+wl_status grad_core(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, const void *x, const void *b, void *g,
+                    double *f_dev, char *w, const WsLayout &L, cudaStream_t s);
 
 }  // namespace
 
@@ -529,6 +544,20 @@ static wl_status residual_core(const wl_blur_plan *bl, int64_t batch, const void
   return WL_OK;
 }
 
+}  // extern "C"
+
+namespace {
+wl_status grad_core(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, const void *x, const void *b, void *g,
+                    double *f_dev, char *w, const WsLayout &L, cudaStream_t s) {
+  wl_status st;
+  if ((st = run_synthesis(p, batch, x, w + L.u, w, L, s))) return st;          // u = W x
+  if ((st = residual_core(bl, batch, w + L.u, b, w + L.s, f_dev, s))) return st;  // s = R*(R u - b)
+  return run_analysis(p, batch, w + L.s, g, w, L, true, s);                     // g = W* s
+}
+}  // namespace
+
+extern "C" {
+
 wl_status wl_blur_residual_adjoint(const wl_blur_plan *bl, int64_t batch, const void *u, const void *b, void *s,
                                    double *f_dev, void *stream) {
   if (!bl) return fail(WL_EINVAL, "blur plan is NULL");
@@ -564,11 +593,98 @@ wl_status wl_grad(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, const
   WsLayout L = ws_layout(p, bl, WL_OP_GRAD, batch);
   if (overlap(ws, L.total, x, xb) || overlap(ws, L.total, g, xb) || overlap(ws, L.total, b, ib))
     return fail(WL_EINVAL, "wl_grad: ws overlaps an argument");
+  st = grad_core(p, bl, batch, x, b, g, f_dev, (char *)ws, L, (cudaStream_t)stream);
+  return st ? st : ok();
+}
+
+wl_status wl_fista_update(const wl_plan *p, int64_t batch, const void *g, void *x, void *y, double t, double lambda,
+                          double lip, void *stream) {
+  if (check_plan(p)) return WL_EINVAL;
+  if (batch < 0) return fail(WL_EINVAL, "wl_fista_update: batch=%lld < 0", (long long)batch);
+  if (!(lip > 0) || !std::isfinite(lip)) return fail(WL_EINVAL, "wl_fista_update: lip=%g must be > 0", lip);
+  if (!(lambda >= 0) || !std::isfinite(lambda)) return fail(WL_EINVAL, "wl_fista_update: lambda=%g must be >= 0", lambda);
+  if (!(t >= 1) || !std::isfinite(t)) return fail(WL_EINVAL, "wl_fista_update: t=%g must be >= 1", t);
+  if (batch == 0) return ok();
+  const size_t xb = (size_t)batch * p->p_alloc * p->es;
+  wl_status st;
+  if ((st = check_dev(g, "g")) || (st = check_dev(x, "x")) || (st = check_dev(y, "y"))) return st;
+  if (overlap(g, xb, x, xb) || overlap(g, xb, y, xb) || overlap(x, xb, y, xb))
+    return fail(WL_EINVAL, "wl_fista_update: g, x and y must not overlap");
+  cudaError_t e = launch_fista_update(p->dtype, g, x, y, (long long)batch * p->p_alloc, t, lambda, lip,
+                                      (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "fista update launch");
+  return ok();
+}
+
+wl_status wl_fista_step(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, const void *b, void *x, void *y,
+                        double t, double lambda, double lip, double *f_dev, void *ws, void *stream) {
+  if (check_plan(p)) return WL_EINVAL;
+  if (!bl) return fail(WL_EINVAL, "wl_fista_step: blur plan is NULL");
+  if (bl->h != p->h || bl->w != p->w || bl->dtype != p->dtype)
+    return fail(WL_EINVAL, "wl_fista_step: blur plan does not match the wavelet plan");
+  if (batch < 0) return fail(WL_EINVAL, "wl_fista_step: batch=%lld < 0", (long long)batch);
+  if (!(lip > 0) || !(lambda >= 0) || !(t >= 1)) return fail(WL_EINVAL, "wl_fista_step: need lip > 0, lambda >= 0, t >= 1");
+  if (batch == 0) return ok();
+  const size_t ib = (size_t)batch * p->h * p->w * p->es, xb = (size_t)batch * p->p_alloc * p->es;
+  wl_status st;
+  if ((st = check_dev(b, "b")) || (st = check_dev(x, "x")) || (st = check_dev(y, "y"))) return st;
+  if (overlap(x, xb, y, xb) || overlap(b, ib, x, xb) || overlap(b, ib, y, xb))
+    return fail(WL_EINVAL, "wl_fista_step: b, x and y must not overlap");
+  if (f_dev && (st = check_dev(f_dev, "f_dev", 8))) return st;
+  if ((st = check_ws(p, bl, WL_OP_FISTA, batch, ws))) return st;
+  WsLayout L = ws_layout(p, bl, WL_OP_FISTA, batch);
+  if (overlap(ws, L.total, x, xb) || overlap(ws, L.total, y, xb) || overlap(ws, L.total, b, ib))
+    return fail(WL_EINVAL, "wl_fista_step: ws overlaps an argument");
   cudaStream_t s = (cudaStream_t)stream;
   char *w = (char *)ws;
-  if ((st = run_synthesis(p, batch, x, w + L.u, w, L, s))) return st;          // u = W x
-  if ((st = residual_core(bl, batch, w + L.u, b, w + L.s, f_dev, s))) return st;  // s = R*(R u - b)
-  if ((st = run_analysis(p, batch, w + L.s, g, w, L, true, s))) return st;     // g = W* s
+  if ((st = grad_core(p, bl, batch, y, b, w + L.g, f_dev, w, L, s))) return st;  // g = grad f(y)
+  cudaError_t e = launch_fista_update(p->dtype, w + L.g, x, y, (long long)batch * p->p_alloc, t, lambda, lip, s);
+  if (e != cudaSuccess) return cuda_fail(e, "fista update launch");
+  return ok();
+}
+
+wl_status wl_lipschitz(const wl_plan *p, const wl_blur_plan *bl, int iters, uint64_t seed, double *lip_host, void *ws,
+                       void *stream) {
+  if (check_plan(p)) return WL_EINVAL;
+  if (!bl) return fail(WL_EINVAL, "wl_lipschitz: blur plan is NULL");
+  if (bl->h != p->h || bl->w != p->w || bl->dtype != p->dtype)
+    return fail(WL_EINVAL, "wl_lipschitz: blur plan does not match the wavelet plan");
+  if (iters < 1) return fail(WL_EINVAL, "wl_lipschitz: iters=%d must be >= 1", iters);
+  if (!lip_host) return fail(WL_EINVAL, "wl_lipschitz: lip_host is NULL");
+  wl_status st;
+  if ((st = check_ws(p, bl, WL_OP_LIPSCHITZ, 1, ws))) return st;
+  WsLayout L = ws_layout(p, bl, WL_OP_LIPSCHITZ, 1);
+  cudaStream_t s = (cudaStream_t)stream;
+  char *w = (char *)ws;
+  void *v = w + L.v, *g = w + L.g, *b0 = w + L.b0;
+  double *d = reinterpret_cast<double *>(w + L.d);
+  const long long n = p->p_alloc;
+  cudaError_t e = cudaMemsetAsync(b0, 0, (size_t)p->h * p->w * p->es, s);
+  if (e == cudaSuccess) e = launch_fill_seeded(p->dtype, v, n, (unsigned long long)seed, s);
+  if (e != cudaSuccess) return cuda_fail(e, "wl_lipschitz init");
+  double est = 0.0;
+  for (int it = 0; it < iters; it++) {
+    double h[2];
+    e = launch_dot(p->dtype, v, v, n, 1, d, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, d, sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "wl_lipschitz norm");
+    if (!(h[0] > 0)) {  // zero operator
+      *lip_host = 0.0;
+      return ok();
+    }
+    e = launch_scale(p->dtype, v, n, 1.0 / std::sqrt(h[0]), s);
+    if (e != cudaSuccess) return cuda_fail(e, "wl_lipschitz scale");
+    if ((st = grad_core(p, bl, 1, v, b0, g, nullptr, w, L, s))) return st;  // g = W* R* R W v
+    e = launch_dot(p->dtype, v, g, n, 1, d + 1, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h + 1, d + 1, sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "wl_lipschitz rayleigh");
+    est = h[1];  // <v, G v> with ||v|| = 1
+    e = cudaMemcpyAsync(v, g, (size_t)n * p->es, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "wl_lipschitz copy");
+  }
+  *lip_host = est;
   return ok();
 }
 

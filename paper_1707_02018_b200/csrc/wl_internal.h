@@ -79,6 +79,12 @@ cudaError_t launch_fold(int dtype, const FoldArgs &a, cudaStream_t s);
 cudaError_t launch_blur(int dtype, const BlurArgs &a, cudaStream_t s);
 cudaError_t launch_blur_residual(int dtype, const BlurArgs &a, cudaStream_t s);
 cudaError_t launch_zero(void *ptr, size_t bytes, cudaStream_t s);
+// FISTA pieces (fista_kernels.cu); n = elements per call (batch * p_alloc for the update)
+cudaError_t launch_fista_update(int dtype, const void *g, void *x, void *y, long long n, double t, double lambda,
+                                double lip, cudaStream_t s);
+cudaError_t launch_dot(int dtype, const void *a, const void *b, long long n, int batch, double *out, cudaStream_t s);
+cudaError_t launch_scale(int dtype, void *v, long long n, double alpha, cudaStream_t s);
+cudaError_t launch_fill_seeded(int dtype, void *v, long long n, unsigned long long seed, cudaStream_t s);
 
 // Encode a 3-D tiled TMA descriptor (CUtensorMap, 128 bytes at `map`) over a tensor of
 // d0 x d1 x d2 elements of `elem_bytes` (4: fp32, 8: fp64) with byte strides s1 (dim 1) and

@@ -23,7 +23,7 @@ _LIB_PATH = os.environ.get("WL_LIB") or os.path.join(_PKG, "libwl.so")   # WL_LI
 WL_OK, WL_EINVAL, WL_ESIZE, WL_EDTYPE, WL_EALIGN, WL_ENOMEM, WL_ECUDA = range(7)
 FILTERS = {"haar": 1, "db1": 1, "db2": 2, "db4": 4, "db8": 8, "cdf97": 97}
 BCS = {"zero": 0, "periodic": 1, "symmetric": 2, "symmetric_edag": 3}
-OP_SYNTHESIZE, OP_ADJOINT, OP_ANALYZE, OP_GRAD, OP_ANALYZE_ADJOINT = range(5)
+OP_SYNTHESIZE, OP_ADJOINT, OP_ANALYZE, OP_GRAD, OP_ANALYZE_ADJOINT, OP_FISTA, OP_LIPSCHITZ = range(7)
 MAX_LEVELS = 32
 
 
@@ -47,7 +47,8 @@ class _PlanInfo(ctypes.Structure):
 EXPORTS = ("wl_plan_create", "wl_plan_destroy", "wl_plan_query", "wl_plan_filters", "wl_workspace_bytes",
            "wl_synthesize", "wl_adjoint", "wl_analyze", "wl_analyze_adjoint", "wl_blur_create", "wl_blur_create_gaussian",
            "wl_blur_destroy", "wl_blur_taps", "wl_blur", "wl_blur_adjoint", "wl_blur_residual_adjoint",
-           "wl_grad", "wl_last_error", "wl_launch_count", "wl_version")
+           "wl_grad", "wl_fista_update", "wl_fista_step", "wl_lipschitz", "wl_last_error", "wl_launch_count",
+           "wl_version")
 
 _lib = None
 
@@ -84,6 +85,9 @@ def lib():
     L.wl_blur_adjoint.argtypes = [vp, i64, vp, vp, vp]
     L.wl_blur_residual_adjoint.argtypes = [vp, i64, vp, vp, vp, vp, vp]
     L.wl_grad.argtypes = [vp, vp, i64, vp, vp, vp, vp, vp, vp]
+    L.wl_fista_update.argtypes = [vp, i64, vp, vp, vp, cd, cd, cd, vp]
+    L.wl_fista_step.argtypes = [vp, vp, i64, vp, vp, vp, cd, cd, cd, vp, vp, vp]
+    L.wl_lipschitz.argtypes = [vp, vp, ci, ctypes.c_uint64, dp, vp, vp]
     L.wl_last_error.restype = ctypes.c_char_p
     L.wl_launch_count.restype = ctypes.c_int64
     L.wl_version.restype = ctypes.c_char_p
@@ -360,3 +364,58 @@ def grad(plan: Plan, blur: Blur, x, b, out=None, f=None, ws=None, stream=None):
     ws = plan._ws(OP_GRAD, B, blur=blur, ws=ws)
     _check(lib().wl_grad(plan._h, blur._h, B, _ptr(x), _ptr(b), _ptr(out), _ptr(f), _ptr(ws), _stream_ptr(stream)))
     return out
+
+
+# ------------------------------------------------------------------ FISTA
+def next_t(t: float) -> float:
+    """FISTA momentum recursion t_{k+1} = (1 + sqrt(1 + 4 t_k^2)) / 2 (host scalar)."""
+    return (1.0 + (1.0 + 4.0 * t * t) ** 0.5) / 2.0
+
+
+def lipschitz(plan: Plan, blur: Blur, iters: int = 50, seed: int = 1, ws=None, stream=None) -> float:
+    """lambda_max(W* R* R W) by power iteration on the GPU (wl_lipschitz; blocking)."""
+    ws = plan._ws(OP_LIPSCHITZ, 1, blur=blur, ws=ws)
+    out = ctypes.c_double()
+    _check(lib().wl_lipschitz(plan._h, blur._h, int(iters), ctypes.c_uint64(seed), ctypes.byref(out), _ptr(ws),
+                              _stream_ptr(stream)))
+    return out.value
+
+
+def fista_update(plan: Plan, g, x, y, t: float, lam: float, lip: float, stream=None):
+    """In place: x <- soft(y - g/lip, lam/lip), y <- x + ((t-1)/t+)(x - x_old); returns t+."""
+    for name, a in (("g", g), ("x", x), ("y", y)):
+        _require(a, name, plan.torch_dtype, (plan.p_alloc,))
+    B = plan._batch_of(x, 1)
+    _check(lib().wl_fista_update(plan._h, B, _ptr(g), _ptr(x), _ptr(y), float(t), float(lam), float(lip),
+                                 _stream_ptr(stream)))
+    return next_t(t)
+
+
+def fista_step(plan: Plan, blur: Blur, b, x, y, t: float, lam: float, lip: float, f=None, ws=None, stream=None):
+    """One FISTA iteration on the GPU (grad f(y) then the fused prox + momentum update); returns t+."""
+    _require(b, "b", plan.torch_dtype, (plan.h, plan.w))
+    _require(x, "x", plan.torch_dtype, (plan.p_alloc,))
+    _require(y, "y", plan.torch_dtype, (plan.p_alloc,))
+    B = plan._batch_of(x, 1)
+    if f is not None:
+        _require(f, "f", _torch().float64)
+    ws = plan._ws(OP_FISTA, B, blur=blur, ws=ws)
+    _check(lib().wl_fista_step(plan._h, blur._h, B, _ptr(b), _ptr(x), _ptr(y), float(t), float(lam), float(lip),
+                               _ptr(f), _ptr(ws), _stream_ptr(stream)))
+    return next_t(t)
+
+
+def fista(plan: Plan, blur: Blur, b, lam: float, iters: int, lip: float = None, x0=None, stream=None):
+    """FISTA for min_x 1/2 ||R W x - b||^2 + lam ||x||_1 (Eq. (1); P:117 runs 2500 iterations).
+    Returns (x, y, t)."""
+    torch = _torch()
+    B = int(np.prod(b.shape[:-2])) if b.dim() > 2 else 1
+    if lip is None:
+        lip = lipschitz(plan, blur, stream=stream)
+    x = torch.zeros(b.shape[:-2] + (plan.p_alloc,), dtype=b.dtype, device=b.device) if x0 is None else x0.clone()
+    y = x.clone()
+    ws = plan._ws(OP_FISTA, B, blur=blur)
+    t = 1.0
+    for _ in range(int(iters)):
+        t = fista_step(plan, blur, b, x, y, t, lam, lip, ws=ws, stream=stream)
+    return x, y, t

@@ -1,0 +1,88 @@
+"""GPU FISTA against the fp64 oracle on identical inputs.
+
+Tolerances (DESIGN.md §3 "FISTA"): the fused update is elementwise, so it matches the oracle's
+update to rounding (fp64 1e-13, fp32 2e-6, like the operators).  K iterations compose K gradients
+and K soft-thresholds; fp64 stays at 1e-11 after 10 iterations; fp32 at 1e-4 (per-iteration
+operator error ~1e-7 relative, grown by the iteration and by coefficients crossing the threshold
+in one precision and not the other).  The power iteration converges to lambda_max of the dense
+(R W)^T (R W) from below.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1707_02018_b200 import inputs, wl
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def dev(torch, a, dtype):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device="cuda", dtype=getattr(torch, dtype))
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.mark.parametrize("dtype,tol", [("float64", 1e-13), ("float32", 2e-6)])
+def test_fista_update_matches_oracle(torch, dtype, tol):
+    plan = wl.Plan(37, 45, 2, "cdf97", "symmetric", dtype)
+    rng = np.random.default_rng(0)
+    B = 2
+    g, x, y = (inputs.cast(rng.standard_normal((B, plan.p_valid)), dtype) for _ in range(3))
+    t, lam, lip = 1.7, 0.3, 2.5
+    xo, yo, to = O.fista_update(g, x, y, t, lam, lip)
+    gd, xd, yd = (dev(torch, plan.from_packed(a), dtype) for a in (g, x, y))
+    t_new = wl.fista_update(plan, gd, xd, yd, t, lam, lip)
+    assert t_new == pytest.approx(to, rel=1e-15)
+    assert rel(plan.to_packed(xd.double().cpu().numpy()), xo) <= tol
+    assert rel(plan.to_packed(yd.double().cpu().numpy()), yo) <= tol
+    pad = np.setdiff1d(np.arange(plan.p_alloc), plan.to_packed(np.arange(plan.p_alloc)[None])[0].astype(np.int64))
+    assert np.all(xd.cpu().numpy()[:, pad] == 0) and np.all(yd.cpu().numpy()[:, pad] == 0)
+
+
+@pytest.mark.parametrize("filt,bc", [("cdf97", "symmetric"), ("haar", "symmetric"), ("db4", "zero")])
+@pytest.mark.parametrize("dtype,tol", [("float64", 1e-11), ("float32", 1e-4)])
+def test_fista_iterations_match_oracle(torch, filt, bc, dtype, tol):
+    h, w, J, B, K = 40, 36, 3, 2, 10
+    plan = wl.Plan(h, w, J, filt, bc, dtype)
+    blur = wl.Blur(h, w, 15, 3.0, dtype=dtype)
+    rng = np.random.default_rng(5)
+    b = inputs.cast(O.blur(inputs.blobs(rng, B, h, w, 8)) + 1e-3 * rng.standard_normal((B, h, w)), dtype)
+    lam, lip = 2e-3, 1.05
+    x, y, t, _ = O.fista(np.zeros((B, plan.p_valid)), b, J, filt, bc, lam, lip, K)
+    xg, yg, tg = wl.fista(plan, blur, dev(torch, b, dtype), lam, K, lip=lip)
+    assert tg == pytest.approx(t, rel=1e-14)
+    assert rel(plan.to_packed(xg.double().cpu().numpy()), x) <= tol
+    assert rel(plan.to_packed(yg.double().cpu().numpy()), y) <= tol
+
+
+def test_fista_zero_solution_when_lambda_large(torch):
+    h, w, J = 32, 32, 2
+    plan = wl.Plan(h, w, J, "db2", "symmetric", "float64")
+    blur = wl.Blur(h, w, 15, 3.0, dtype="float64")
+    b = np.random.default_rng(1).standard_normal((1, h, w))
+    lam = 1.01 * np.abs(O.grad(np.zeros((1, plan.p_valid)), b, J, "db2", "symmetric")[0]).max()
+    xg, _, _ = wl.fista(plan, blur, dev(torch, b, "float64"), lam, 5, lip=1.0)
+    assert float(xg.abs().max()) == 0.0
+
+
+def test_lipschitz_matches_dense_eigenvalue(torch):
+    h, w, J, filt, bc = 12, 10, 2, "db2", "symmetric"
+    plan = wl.Plan(h, w, J, filt, bc, "float64")
+    blur = wl.Blur(h, w, 15, 3.0, dtype="float64")
+    p = plan.p_valid
+    Wm = O.synthesize(np.eye(p), h, w, J, filt, bc).reshape(p, h * w)
+    RW = np.stack([O.blur(Wm[i].reshape(h, w)).ravel() for i in range(p)], 1)
+    lmax = np.linalg.eigvalsh(RW.T @ RW).max()
+    est = wl.lipschitz(plan, blur, iters=300, seed=3)
+    assert est <= lmax * (1 + 1e-10)
+    assert abs(est - lmax) <= 1e-8 * lmax
