@@ -274,6 +274,14 @@ def run_wl(args):
              "bytes": b4, "config": "cfg4 4096^2 db8 zero 6 levels fp32"}
     del y4, x4, ws4
 
+    # ---- one FISTA iteration at cfg5 (grad f(y) + fused prox/momentum update)
+    xf, yf = torch.zeros_like(x), x.clone()
+    wsf = plan._ws(wl.OP_FISTA, B, blur=blur)
+    tf = time_calls(torch, lambda: wl.fista_step(plan, blur, b, xf, yf, 2.0, 1e-3, 1.0, ws=wsf), reps)
+    fista = {"ms_per_iter": tf, "iters_per_s": ws / (tf * 1e-3), "update_overhead_ms": tf - ms,
+             "config": "cfg5, lambda 1e-3, L 1"}
+    del xf, yf, wsf
+
     # ---- end to end through the public API with host buffers (pinned), copies inside
     xh = x.cpu().pin_memory()
     bh = b.cpu().pin_memory()
@@ -319,7 +327,7 @@ def run_wl(args):
                            "bytes_per_step_per_gpu": nbytes},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(), "grad_evals_per_s": ws / (ms * 1e-3), "images_per_s": ws * B / (ms * 1e-3),
-                "grad_frac_of_hbm_roofline": value / ws / hbm_peak, "wstar_cfg4": wstar, "kernels": kernels}
+                "grad_frac_of_hbm_roofline": value / ws / hbm_peak, "wstar_cfg4": wstar, "fista_cfg5": fista, "kernels": kernels}
         print(json.dumps(line))
     if ws > 1:
         import torch.distributed as dist

@@ -17,7 +17,9 @@
 //      (L-2 carried rows + 2G new);
 //   C  axis-0 pass: each thread owns a column pair of one history and produces VC coefficient
 //      rows of two subbands (X = lo, hi) from a register window, stored as float2 pairs
-//      (padding columns of the pitched rows written as 0).
+//      (padding columns of the pitched rows written as 0).  With the FISTA epilogue (FU) the
+//      coefficient pair is not stored: it is g of grad f(y), and the store becomes the prox +
+//      momentum update of (x, y) in place (prox fused into W*'s store).
 // Loops run tap-outer so only one tap pair is live at a time (no register spills).
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -83,7 +85,14 @@ struct ACfg {
   static constexpr size_t OFF_U = 0;  // [NS][GI][UP]
   static constexpr size_t OFF_H = OFF_U + round_up_c(NS * GI * UP * (int)sizeof(T), 128);  // [2 sets][HR][HP]
   static constexpr size_t OFF_BAR = OFF_H + 2 * (size_t)HR * HP * sizeof(T);
-  static constexpr size_t smem_bytes() { return OFF_BAR + NS * sizeof(uint64_t); }
+  // FISTA epilogue (FU): per stage, the (y, x) tiles of the block's G coefficient rows x TQ
+  // columns for the 4 subbands, prefetched by cp.async with the input rows (no load latency
+  // in the store stage)
+  static constexpr int FT = G * TQ;                      // elements per (subband, array) tile
+  static constexpr size_t OFF_F = round_up_c(OFF_BAR + NS * sizeof(uint64_t), 128);  // [NS][4][2][G][TQ]
+  static constexpr size_t smem_bytes(bool fu = false) {
+    return fu ? OFF_F + (size_t)NS * 8 * FT * sizeof(T) : OFF_BAR + NS * sizeof(uint64_t);
+  }
 };
 
 template <typename T, int L>
@@ -101,9 +110,37 @@ struct AnaStreamParams {
   T flo[L], fhi[L];          // raw taps (gather weights)
   P fb[L];                   // B tap pairs (f_lo[j], f_hi[j])
   P slo[L], shi[L];          // C broadcast taps (f[j], f[j])
+  // fused FISTA epilogue (FU): for subbands in fmask the output pointer is y; x = y + xdelta.
+  // The W* value g never reaches HBM:  x+ = soft(y - g/L, lambda/L), y+ = x+ + mom (x+ - x)
+  int fmask;
+  long long xdelta;
+  T inv_lip, tau, mom;
 };
 
+template <typename T>
+__device__ __forceinline__ T soft_thr(T v, T tau) {
+  const T a = v > T(0) ? v : -v;
+  const T m = a - tau;
+  return m > T(0) ? (v > T(0) ? m : -m) : T(0);
+}
+
+// fused FISTA update of one coefficient pair: g of grad f(y); (y, x) old values from the
+// prefetched tile; writes x+ and y+ at yp and yp + xdelta
 template <typename T, int L>
+__device__ __forceinline__ void fista_pair(const AnaStreamParams<T, L> &p, T *yp, typename Pair<T>::t g,
+                                           const T *tile_y, const T *tile_x) {
+  using P = typename Pair<T>::t;
+  const P yv = *reinterpret_cast<const P *>(tile_y), xv = *reinterpret_cast<const P *>(tile_x);
+  P xn, yn;
+  xn.x = soft_thr<T>(yv.x - g.x * p.inv_lip, p.tau);
+  xn.y = soft_thr<T>(yv.y - g.y * p.inv_lip, p.tau);
+  yn.x = xn.x + p.mom * (xn.x - xv.x);
+  yn.y = xn.y + p.mom * (xn.y - xv.y);
+  *reinterpret_cast<P *>(yp + p.xdelta) = xn;
+  *reinterpret_cast<P *>(yp) = yn;
+}
+
+template <typename T, int L, bool FU>
 __global__ void __launch_bounds__(ACfg<T, L>::NT, sizeof(T) == 4 ? 768 / ACfg<T, L>::NT : 1)
     k_ana_stream(const __grid_constant__ AnaStreamParams<T, L> p) {
   using C = ACfg<T, L>;
@@ -114,6 +151,7 @@ __global__ void __launch_bounds__(ACfg<T, L>::NT, sizeof(T) == 4 ? 768 / ACfg<T,
   T *ubuf = reinterpret_cast<T *>(smem_raw + C::OFF_U);  // [NS][GI][UP] input rows
   T *hist = reinterpret_cast<T *>(smem_raw + C::OFF_H);  // [2][HR][HP] lo / hi coefficient columns
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + C::OFF_BAR);
+  T *ftile = reinterpret_cast<T *>(smem_raw + C::OFF_F);  // FU only: [NS][4][2 (y, x)][G][TQ]
 
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -144,12 +182,25 @@ __global__ void __launch_bounds__(ACfg<T, L>::NT, sizeof(T) == 4 ? 768 / ACfg<T,
     T *oX0 = p.out[setC] + (long long)img * p.out_bstride[setC];          // X = lo: LL or LH
     T *oX1 = p.out[setC + 2] + (long long)img * p.out_bstride[setC + 2];  // X = hi: HL or HH
     const long long pX0 = p.out_pitch[setC], pX1 = p.out_pitch[setC + 2];
+    const bool fu0 = FU && ((p.fmask >> setC) & 1), fu1 = FU && ((p.fmask >> (setC + 2)) & 1);
 
     // input block b (b = -1 .. nblk-1): rows 2(kr0 + bG) .. +2G -> ubuf[(b + 1) % NS]
     auto load_block = [&](int b) -> bool {
       const int r_in = 2 * (kr0 + b * G);
       const int sl = (b + 1) % C::NS;
       T *dst0 = ubuf + sl * GI * C::UP;
+      if (FU && b >= 0) {  // (y, x) tiles of coefficient rows kr0 + bG .. for the fused update
+        constexpr int CPR = TQ / VEC;
+        T *fdst = ftile + sl * 8 * C::FT;
+        for (int idx = tid; idx < 8 * G * CPR; idx += C::NT) {
+          const int c = idx % CPR, r = (idx / CPR) % G, arr = (idx / (CPR * G)) & 1, band = idx / (2 * CPR * G);
+          const int kr = kr0 + b * G + r, col = q0 + c * VEC;
+          if (!((p.fmask >> band) & 1) || kr >= kr1 || col >= p.out_pitch[band]) continue;
+          const T *src = p.out[band] + (long long)img * p.out_bstride[band] + (long long)kr * p.out_pitch[band] + col +
+                         (arr ? p.xdelta : 0);
+          cp_async16(fdst + ((band * 2 + arr) * G + r) * TQ + c * VEC, src);
+        }
+      }
       const bool inside = r_in >= 0 && r_in + GI <= p.n0 && cbox >= 0 && cbox + C::UW <= p.n1;
       if (p.tma && (p.tma_any_block || inside)) {
         if (tid == 0) {
@@ -258,11 +309,23 @@ __global__ void __launch_bounds__(ACfg<T, L>::NT, sizeof(T) == 4 ? 768 / ACfg<T,
         }
         // pitched rows: columns [m1, pitch) are padding written as 0; qc is even and so is
         // every pitch, so a pair never straddles the pitch
+        // FU: this item's (y, x) tile entries: subband setC / setC + 2, row grpC*VC + v, column 2 mC
+        const T *ft0 = ftile + (slot * 8 + setC * 2) * C::FT + (grpC * VC) * TQ + 2 * mC;
+        const T *ft1 = ftile + (slot * 8 + (setC + 2) * 2) * C::FT + (grpC * VC) * TQ + 2 * mC;
         const bool in0 = qc < p.m1, in1 = qc + 1 < p.m1;
         const bool st0 = qc < pX0;
         if (in1 && krb + VC <= kr1) {  // fast path: whole item inside the band and the image
           T *d0 = oX0 + (long long)krb * pX0 + qc;
           T *d1 = oX1 + (long long)krb * pX1 + qc;
+          if (FU && (fu0 || fu1)) {
+#pragma unroll
+            for (int v = 0; v < VC; v++) {
+              if (fu0) fista_pair<T, L>(p, d0 + v * pX0, a0[v], ft0 + v * TQ, ft0 + C::FT + v * TQ);
+              else *reinterpret_cast<P *>(d0 + v * pX0) = a0[v];
+              if (fu1) fista_pair<T, L>(p, d1 + v * pX1, a1[v], ft1 + v * TQ, ft1 + C::FT + v * TQ);
+              else *reinterpret_cast<P *>(d1 + v * pX1) = a1[v];
+            }
+          } else
 #pragma unroll
           for (int v = 0; v < VC; v++) {
             *reinterpret_cast<P *>(d0 + v * pX0) = a0[v];
@@ -276,8 +339,21 @@ __global__ void __launch_bounds__(ACfg<T, L>::NT, sizeof(T) == 4 ? 768 / ACfg<T,
           P z0 = a0[v], z1 = a1[v];
           if (!in0) z0.x = z1.x = T(0);
           if (!in1) z0.y = z1.y = T(0);
-          *reinterpret_cast<P *>(oX0 + (long long)kr * pX0 + qc) = z0;
-          *reinterpret_cast<P *>(oX1 + (long long)kr * pX1 + qc) = z1;
+          T *e0 = oX0 + (long long)kr * pX0 + qc, *e1 = oX1 + (long long)kr * pX1 + qc;
+          if (FU && fu0) {  // padding entries of x and y stay 0
+            fista_pair<T, L>(p, e0, z0, ft0 + v * TQ, ft0 + C::FT + v * TQ);
+            if (!in0) e0[0] = e0[p.xdelta] = T(0);
+            if (!in1) e0[1] = e0[p.xdelta + 1] = T(0);
+          } else {
+            *reinterpret_cast<P *>(e0) = z0;
+          }
+          if (FU && fu1) {
+            fista_pair<T, L>(p, e1, z1, ft1 + v * TQ, ft1 + C::FT + v * TQ);
+            if (!in0) e1[0] = e1[p.xdelta] = T(0);
+            if (!in1) e1[1] = e1[p.xdelta + 1] = T(0);
+          } else {
+            *reinterpret_cast<P *>(e1) = z1;
+          }
         }
       }
       __syncthreads();  // (3) history readers done
@@ -294,7 +370,7 @@ __global__ void __launch_bounds__(ACfg<T, L>::NT, sizeof(T) == 4 ? 768 / ACfg<T,
   }
 }
 
-template <typename T, int L>
+template <typename T, int L, bool FU>
 cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
   using C = ACfg<T, L>;
   AnaStreamParams<T, L> p;
@@ -327,9 +403,14 @@ cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
     p.slo[j].x = p.slo[j].y = T(a.lo[j]);
     p.shi[j].x = p.shi[j].y = T(a.hi[j]);
   }
+  p.fmask = a.fista_mask;
+  p.xdelta = a.fista_xdelta;
+  p.inv_lip = T(a.fista_inv_lip);
+  p.tau = T(a.fista_tau);
+  p.mom = T(a.fista_mom);
   p.nstrips = (a.m1 + C::TQ - 1) / C::TQ;
-  const size_t smem = C::smem_bytes();
-  auto kern = k_ana_stream<T, L>;
+  const size_t smem = C::smem_bytes(FU);
+  auto kern = k_ana_stream<T, L, FU>;
   long long resident = 0;
   cudaError_t e = kernel_resident(reinterpret_cast<const void *>(kern), C::NT, smem, &resident);
   if (e != cudaSuccess) return e;
@@ -343,13 +424,20 @@ cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
 
 template <typename T>
 cudaError_t dispatch(const AnalysisArgs &a, cudaStream_t s) {
-  switch (a.L) {
-    case 2: return launch_ana_stream_t<T, 2>(a, s);
-    case 4: return launch_ana_stream_t<T, 4>(a, s);
-    case 8: return launch_ana_stream_t<T, 8>(a, s);
-    case 10: return launch_ana_stream_t<T, 10>(a, s);
-    case 16: return launch_ana_stream_t<T, 16>(a, s);
-  }
+  if (a.fista_mask) switch (a.L) {
+      case 2: return launch_ana_stream_t<T, 2, true>(a, s);
+      case 4: return launch_ana_stream_t<T, 4, true>(a, s);
+      case 8: return launch_ana_stream_t<T, 8, true>(a, s);
+      case 10: return launch_ana_stream_t<T, 10, true>(a, s);
+      case 16: return launch_ana_stream_t<T, 16, true>(a, s);
+    }
+  else switch (a.L) {
+      case 2: return launch_ana_stream_t<T, 2, false>(a, s);
+      case 4: return launch_ana_stream_t<T, 4, false>(a, s);
+      case 8: return launch_ana_stream_t<T, 8, false>(a, s);
+      case 10: return launch_ana_stream_t<T, 10, false>(a, s);
+      case 16: return launch_ana_stream_t<T, 16, false>(a, s);
+    }
   return cudaErrorInvalidValue;
 }
 

@@ -146,8 +146,15 @@ Buf band_buf(const wl_plan *p, const void *x, int idx) {
 int lh_index(const wl_plan *p, int j) { return 1 + 3 * (p->J - j); }
 
 // analysis chain (W-dagger when adjoint = false, W* when true) -----------------
+// fused FISTA epilogue for the W* chain: x is the coefficient array written by run_analysis (= y of
+// the iteration), xo the other state vector; every stored coefficient is g of grad f(y).
+struct FistaFuse {
+  void *xo;
+  double inv_lip, tau, mom;
+};
+
 wl_status run_analysis(const wl_plan *p, int64_t batch, const void *img, void *x, char *ws, const WsLayout &L,
-                       bool adjoint, cudaStream_t s) {
+                       bool adjoint, cudaStream_t s, const FistaFuse *fz = nullptr) {
   int ext;
   if (adjoint)
     ext = p->bc == WL_BC_PERIODIC ? EXT_PER : (p->bc == WL_BC_SYMMETRIC_EDAG ? EXT_SYM_PADJ : EXT_ZERO);
@@ -183,6 +190,13 @@ wl_status run_analysis(const wl_plan *p, int64_t batch, const void *img, void *x
     a.hi = adjoint ? p->fb.d_hi : p->fb.a_hi;
     a.L = p->fb.L;
     a.batch = (int)batch;
+    if (fz) {  // LH/HL/HH of every level and LL of the last land in x
+      a.fista_mask = (j == p->J) ? 15 : 14;
+      a.fista_xdelta = ((char *)fz->xo - (char *)x) / (int64_t)p->es;
+      a.fista_inv_lip = fz->inv_lip;
+      a.fista_tau = fz->tau;
+      a.fista_mom = fz->mom;
+    }
     cudaError_t e = launch_analysis(p->dtype, a, s);
     if (e != cudaSuccess) return cuda_fail(e, "analysis level launch");
   }
@@ -637,9 +651,13 @@ wl_status wl_fista_step(const wl_plan *p, const wl_blur_plan *bl, int64_t batch,
     return fail(WL_EINVAL, "wl_fista_step: ws overlaps an argument");
   cudaStream_t s = (cudaStream_t)stream;
   char *w = (char *)ws;
-  if ((st = grad_core(p, bl, batch, y, b, w + L.g, f_dev, w, L, s))) return st;  // g = grad f(y)
-  cudaError_t e = launch_fista_update(p->dtype, w + L.g, x, y, (long long)batch * p->p_alloc, t, lambda, lip, s);
-  if (e != cudaSuccess) return cuda_fail(e, "fista update launch");
+  // g = grad f(y) = W* R* (R W y - b), with the prox + momentum update fused into W*'s stores
+  // (g never reaches HBM).  W reads y before the W* chain rewrites it (stream order).
+  if ((st = run_synthesis(p, batch, y, w + L.u, w, L, s))) return st;
+  if ((st = residual_core(bl, batch, w + L.u, b, w + L.s, f_dev, s))) return st;
+  const double t_new = (1.0 + std::sqrt(1.0 + 4.0 * t * t)) / 2.0;
+  const FistaFuse fz{x, 1.0 / lip, lambda / lip, (t - 1.0) / t_new};
+  if ((st = run_analysis(p, batch, w + L.s, y, w, L, true, s, &fz))) return st;
   return ok();
 }
 

@@ -36,6 +36,10 @@ struct AnalysisArgs {
   const double *lo, *hi;
   int L;
   int batch;
+  // fused FISTA epilogue (0 = plain store): bit i set -> out[i] is y and x = y + fista_xdelta
+  int fista_mask = 0;
+  int64_t fista_xdelta = 0;
+  double fista_inv_lip = 0, fista_tau = 0, fista_mom = 0;
 };
 
 struct SynthesisArgs {

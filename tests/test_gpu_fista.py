@@ -86,3 +86,35 @@ def test_lipschitz_matches_dense_eigenvalue(torch):
     est = wl.lipschitz(plan, blur, iters=300, seed=3)
     assert est <= lmax * (1 + 1e-10)
     assert abs(est - lmax) <= 1e-8 * lmax
+
+
+@pytest.mark.parametrize("filt,bc", [("cdf97", "symmetric"), ("db2", "periodic"), ("db4", "symmetric_edag"),
+                                     ("db8", "zero")])
+@pytest.mark.parametrize("dtype,tol", [("float64", 1e-13), ("float32", 2e-6)])
+def test_fused_step_equals_grad_then_update(torch, filt, bc, dtype, tol):
+    """wl_fista_step fuses the update into W*'s stores; it must equal wl_grad + wl_fista_update
+    (and the oracle's step) from arbitrary (x, y), with the pitch padding left at 0."""
+    h, w, J, B = 72, 56, 3, 2
+    plan = wl.Plan(h, w, J, filt, bc, dtype)
+    blur = wl.Blur(h, w, 15, 3.0, dtype=dtype)
+    rng = np.random.default_rng(11)
+    b = inputs.cast(rng.standard_normal((B, h, w)), dtype)
+    x0, y0 = (inputs.cast(rng.standard_normal((B, plan.p_valid)), dtype) for _ in range(2))
+    t, lam, lip = 3.0, 0.05, 1.3
+    xd, yd = dev(torch, plan.from_packed(x0), dtype), dev(torch, plan.from_packed(y0), dtype)
+    bd = dev(torch, b, dtype)
+    g = wl.grad(plan, blur, yd, bd)
+    xu, yu = xd.clone(), yd.clone()
+    wl.fista_update(plan, g, xu, yu, t, lam, lip)
+    wl.fista_step(plan, blur, bd, xd, yd, t, lam, lip)
+    assert bool(torch.isfinite(xd).all()) and bool(torch.isfinite(yd).all())
+    if dtype == "float64":
+        assert float((xd - xu).abs().max()) <= 1e-13 * float(xu.abs().max())
+        assert float((yd - yu).abs().max()) <= 1e-13 * float(yu.abs().max())
+    go, _ = O.grad(y0.astype(np.float64), b.astype(np.float64), J, filt, bc)
+    xo, yo, _ = O.fista_update(go, x0.astype(np.float64), y0.astype(np.float64), t, lam, lip)
+    assert rel(plan.to_packed(xd.double().cpu().numpy()), xo) <= tol
+    assert rel(plan.to_packed(yd.double().cpu().numpy()), yo) <= tol
+    valid = np.zeros(plan.p_alloc, bool)
+    valid[plan.to_packed(np.arange(plan.p_alloc)[None].astype(np.float64))[0].astype(np.int64)] = True
+    assert np.all(xd.cpu().numpy()[:, ~valid] == 0) and np.all(yd.cpu().numpy()[:, ~valid] == 0)
