@@ -199,6 +199,16 @@ WL_API wl_status wl_blur_residual_adjoint(const wl_blur_plan *blur, int64_t batc
 WL_API wl_status wl_grad(const wl_plan *plan, const wl_blur_plan *blur, int64_t batch, const void *x,
                   const void *b, void *g, double *f_dev, void *ws, void *stream);
 
+/* Which operator closes the gradient (P:117, P:176-177 compare both under FISTA):
+ *   WL_ADJ_TRUE  W*  (the true adjoint, Eq. (4)) -> grad f exactly;
+ *   WL_ADJ_PINV  W-dagger in place of W* (the common approximation W* ~ W-dagger);
+ *                identical to WL_ADJ_TRUE for orthogonal filters under zero / periodic BC. */
+typedef enum { WL_ADJ_TRUE = 0, WL_ADJ_PINV = 1 } wl_adj;
+
+/* wl_grad with the choice of closing operator: g = A R* (R W x - b), A = W* or W-dagger. */
+WL_API wl_status wl_grad_adj(const wl_plan *plan, const wl_blur_plan *blur, int64_t batch, const void *x,
+                      const void *b, void *g, double *f_dev, wl_adj adj, void *ws, void *stream);
+
 /* ------------------------------------------------------------- FISTA */
 
 /* FISTA (Beck & Teboulle 2009; the solver of P:117 and P:174, 2500 iterations there) for
@@ -211,10 +221,12 @@ WL_API wl_status wl_grad(const wl_plan *plan, const wl_blur_plan *blur, int64_t 
  * Pitch padding stays 0.  x, y, g must not overlap (WL_EINVAL). */
 WL_API wl_status wl_fista_update(const wl_plan *plan, int64_t batch, const void *g, void *x, void *y, double t,
                           double lambda, double lip, void *stream);
-/* One full FISTA iteration: g = grad f(y) (wl_grad; f_dev, nullable, receives f(y)), then
- * wl_fista_update.  ws: wl_workspace_bytes(plan, blur, WL_OP_FISTA, batch). */
+/* One full FISTA iteration: g = grad f(y) (wl_grad_adj with `adj`; f_dev, nullable, receives
+ * f(y)), then the wl_fista_update arithmetic, fused into the stores of the closing analysis
+ * chain: g itself is never written.  ws: wl_workspace_bytes(plan, blur, WL_OP_FISTA, batch). */
 WL_API wl_status wl_fista_step(const wl_plan *plan, const wl_blur_plan *blur, int64_t batch, const void *b, void *x,
-                        void *y, double t, double lambda, double lip, double *f_dev, void *ws, void *stream);
+                        void *y, double t, double lambda, double lip, double *f_dev, wl_adj adj, void *ws,
+                        void *stream);
 /* Power iteration for lip = lambda_max(W* R* R W): v_0 = a seeded uniform(-1, 1)
  * vector, v <- G v with G v = grad f(v) at b = 0, estimate <v, G v> / <v, v> of the last step
  * (a lower bound that increases to lambda_max).  Blocking: synchronises `stream` every iteration

@@ -190,6 +190,9 @@ def adjoint(img, J: int, filt: str, bc: str) -> np.ndarray:
     return _analysis(img, J, fb.d_lo, fb.d_hi, fb.L, ext)
 
 
+_adjoint_op = adjoint  # grad's `adjoint` argument shadows the name
+
+
 def synthesize(x, h: int, w: int, J: int, filt: str, bc: str) -> np.ndarray:
     """W = (W*)^T: scatter with the dual filters, then the fold adjoint to W*'s extension."""
     fb = filter_bank(filt)
@@ -226,17 +229,18 @@ def blur_adjoint(img, taps=None) -> np.ndarray:
     return out[0] if squeeze else out
 
 
-def grad(x, b, J: int, filt: str, bc: str, taps=None):
+def grad(x, b, J: int, filt: str, bc: str, taps=None, adjoint: str = "true"):
     """grad f(x) = W* R* (R W x - b) and f = 1/2 ||R W x - b||^2 per image.
 
-    Evaluated literally, in that order, in fp64.
+    Evaluated literally, in that order, in fp64.  adjoint="pinv" replaces W* by W-dagger, the
+    approximation W* ~ W-dagger that P:113-117 and P:176-177 run FISTA with.
     """
     b = _f64(b)
     h, w = b.shape[-2:]
     u = synthesize(x, h, w, J, filt, bc)
     r = blur(u, taps) - b
     s = blur_adjoint(r, taps)
-    g = adjoint(s, J, filt, bc)
+    g = _adjoint_op(s, J, filt, bc) if adjoint == "true" else analyze(s, J, filt, bc)
     f = 0.5 * np.sum(r.reshape(r.shape[:-2] + (-1,)) ** 2, axis=-1)
     return g, f
 
@@ -257,7 +261,7 @@ def fista_update(g, x, y, t, lam, lip):
     return x_new, y_new, t_new
 
 
-def fista(x0, b, J: int, filt: str, bc: str, lam: float, lip: float, iters: int, taps=None):
+def fista(x0, b, J: int, filt: str, bc: str, lam: float, lip: float, iters: int, taps=None, adjoint: str = "true"):
     """FISTA on min_x 1/2 ||R W x - b||^2 + lam ||x||_1 (Eq. (1)): `iters` steps from x0,
     y_1 = x0, t_1 = 1.  Returns (x, y, t, objective trace F(x_k))."""
     x = np.array(x0, dtype=np.float64)
@@ -265,7 +269,7 @@ def fista(x0, b, J: int, filt: str, bc: str, lam: float, lip: float, iters: int,
     t = 1.0
     trace = []
     for _ in range(iters):
-        g, _f = grad(y, b, J, filt, bc, taps)
+        g, _f = grad(y, b, J, filt, bc, taps, adjoint)
         x, y, t = fista_update(g, x, y, t, lam, lip)
         _g, fx = grad(x, b, J, filt, bc, taps)
         trace.append(fx + lam * np.abs(x).reshape(x.shape[0] if x.ndim > 1 else 1, -1).sum(axis=-1))

@@ -300,9 +300,10 @@ wl_status check_io(const void *in, size_t in_bytes, const char *in_name, const v
   return WL_OK;
 }
 
-// g = W* R* (R W x - b) into g (W chain -> fused residual -> W* chain), no validation.
+// g = W* R* (R W x - b) into g (W chain -> fused residual -> W* chain; W-dagger chain when
+// true_adjoint = false), no validation.
 wl_status grad_core(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, const void *x, const void *b, void *g,
-                    double *f_dev, char *w, const WsLayout &L, cudaStream_t s);
+                    double *f_dev, char *w, const WsLayout &L, cudaStream_t s, bool true_adjoint = true);
 
 }  // namespace
 
@@ -562,11 +563,11 @@ static wl_status residual_core(const wl_blur_plan *bl, int64_t batch, const void
 
 namespace {
 wl_status grad_core(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, const void *x, const void *b, void *g,
-                    double *f_dev, char *w, const WsLayout &L, cudaStream_t s) {
+                    double *f_dev, char *w, const WsLayout &L, cudaStream_t s, bool true_adjoint) {
   wl_status st;
   if ((st = run_synthesis(p, batch, x, w + L.u, w, L, s))) return st;          // u = W x
   if ((st = residual_core(bl, batch, w + L.u, b, w + L.s, f_dev, s))) return st;  // s = R*(R u - b)
-  return run_analysis(p, batch, w + L.s, g, w, L, true, s);                     // g = W* s
+  return run_analysis(p, batch, w + L.s, g, w, L, true_adjoint, s);             // g = W* s (or W-dagger s)
 }
 }  // namespace
 
@@ -589,7 +590,13 @@ wl_status wl_blur_residual_adjoint(const wl_blur_plan *bl, int64_t batch, const 
 
 wl_status wl_grad(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, const void *x, const void *b, void *g,
                   double *f_dev, void *ws, void *stream) {
+  return wl_grad_adj(p, bl, batch, x, b, g, f_dev, WL_ADJ_TRUE, ws, stream);
+}
+
+wl_status wl_grad_adj(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, const void *x, const void *b, void *g,
+                      double *f_dev, wl_adj adj, void *ws, void *stream) {
   if (check_plan(p)) return WL_EINVAL;
+  if (adj != WL_ADJ_TRUE && adj != WL_ADJ_PINV) return fail(WL_EINVAL, "wl_grad: adj=%d is not a wl_adj", (int)adj);
   if (!bl) return fail(WL_EINVAL, "wl_grad: blur plan is NULL");
   if (bl->h != p->h || bl->w != p->w)
     return fail(WL_EINVAL, "wl_grad: blur plan is %lldx%lld but wavelet plan is %lldx%lld", (long long)bl->h,
@@ -607,7 +614,7 @@ wl_status wl_grad(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, const
   WsLayout L = ws_layout(p, bl, WL_OP_GRAD, batch);
   if (overlap(ws, L.total, x, xb) || overlap(ws, L.total, g, xb) || overlap(ws, L.total, b, ib))
     return fail(WL_EINVAL, "wl_grad: ws overlaps an argument");
-  st = grad_core(p, bl, batch, x, b, g, f_dev, (char *)ws, L, (cudaStream_t)stream);
+  st = grad_core(p, bl, batch, x, b, g, f_dev, (char *)ws, L, (cudaStream_t)stream, adj == WL_ADJ_TRUE);
   return st ? st : ok();
 }
 
@@ -631,8 +638,9 @@ wl_status wl_fista_update(const wl_plan *p, int64_t batch, const void *g, void *
 }
 
 wl_status wl_fista_step(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, const void *b, void *x, void *y,
-                        double t, double lambda, double lip, double *f_dev, void *ws, void *stream) {
+                        double t, double lambda, double lip, double *f_dev, wl_adj adj, void *ws, void *stream) {
   if (check_plan(p)) return WL_EINVAL;
+  if (adj != WL_ADJ_TRUE && adj != WL_ADJ_PINV) return fail(WL_EINVAL, "wl_fista_step: adj=%d is not a wl_adj", (int)adj);
   if (!bl) return fail(WL_EINVAL, "wl_fista_step: blur plan is NULL");
   if (bl->h != p->h || bl->w != p->w || bl->dtype != p->dtype)
     return fail(WL_EINVAL, "wl_fista_step: blur plan does not match the wavelet plan");
@@ -657,7 +665,7 @@ wl_status wl_fista_step(const wl_plan *p, const wl_blur_plan *bl, int64_t batch,
   if ((st = residual_core(bl, batch, w + L.u, b, w + L.s, f_dev, s))) return st;
   const double t_new = (1.0 + std::sqrt(1.0 + 4.0 * t * t)) / 2.0;
   const FistaFuse fz{x, 1.0 / lip, lambda / lip, (t - 1.0) / t_new};
-  if ((st = run_analysis(p, batch, w + L.s, y, w, L, true, s, &fz))) return st;
+  if ((st = run_analysis(p, batch, w + L.s, y, w, L, adj == WL_ADJ_TRUE, s, &fz))) return st;
   return ok();
 }
 

@@ -92,6 +92,32 @@ def blobs(g: np.random.Generator, batch: int, h: int, w: int, n: int = N_BLOBS) 
     return out
 
 
+def chart(h: int, w: int) -> np.ndarray:
+    """Synthetic resolution-chart stand-in for the Weber 1993 test chart of P:104-110 (the chart
+    itself is not in this container): fp64 [h, w] in [0, 1], background 0.  Groups of vertical and
+    horizontal bar triplets with periods 2..32 px, four disks of decreasing radius and a grey ramp."""
+    img = np.zeros((h, w))
+    periods = [32, 24, 16, 12, 8, 6, 4, 3, 2]
+    gx = w // (len(periods) + 1)
+    for i, per in enumerate(periods):               # vertical bars, top band
+        x0 = gx // 2 + i * gx
+        for k in range(3):
+            a = x0 + 2 * k * (per // 2 if per > 2 else 1)
+            img[h // 16: h // 3, a: a + max(per // 2, 1)] = 1.0
+    gy = h // (len(periods) + 1)
+    for i, per in enumerate(periods):               # horizontal bars, left band of the lower half
+        y0 = h // 3 + gy // 4 + i * (2 * h // 3) // (len(periods) + 1)
+        for k in range(3):
+            a = y0 + 2 * k * (per // 2 if per > 2 else 1)
+            img[a: a + max(per // 2, 1), w // 16: w // 3] = 1.0
+    yy, xx = np.mgrid[0:h, 0:w]
+    for i, r in enumerate([h / 8, h / 12, h / 20, h / 40]):   # disks
+        cy, cx = h / 2 + (i // 2) * h / 4, w / 2 + (i % 2) * w / 4
+        img[(yy - cy) ** 2 + (xx - cx) ** 2 <= r * r] = 0.75
+    img[h - h // 10:, w // 2:] = np.linspace(0.0, 1.0, w - w // 2)[None, :]  # ramp
+    return img
+
+
 def noise(g: np.random.Generator, batch: int, h: int, w: int) -> np.ndarray:
     return NOISE_STD * g.standard_normal((batch, h, w))
 

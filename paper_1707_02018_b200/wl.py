@@ -47,7 +47,7 @@ class _PlanInfo(ctypes.Structure):
 EXPORTS = ("wl_plan_create", "wl_plan_destroy", "wl_plan_query", "wl_plan_filters", "wl_workspace_bytes",
            "wl_synthesize", "wl_adjoint", "wl_analyze", "wl_analyze_adjoint", "wl_blur_create", "wl_blur_create_gaussian",
            "wl_blur_destroy", "wl_blur_taps", "wl_blur", "wl_blur_adjoint", "wl_blur_residual_adjoint",
-           "wl_grad", "wl_fista_update", "wl_fista_step", "wl_lipschitz", "wl_last_error", "wl_launch_count",
+           "wl_grad", "wl_grad_adj", "wl_fista_update", "wl_fista_step", "wl_lipschitz", "wl_last_error", "wl_launch_count",
            "wl_version")
 
 _lib = None
@@ -86,7 +86,8 @@ def lib():
     L.wl_blur_residual_adjoint.argtypes = [vp, i64, vp, vp, vp, vp, vp]
     L.wl_grad.argtypes = [vp, vp, i64, vp, vp, vp, vp, vp, vp]
     L.wl_fista_update.argtypes = [vp, i64, vp, vp, vp, cd, cd, cd, vp]
-    L.wl_fista_step.argtypes = [vp, vp, i64, vp, vp, vp, cd, cd, cd, vp, vp, vp]
+    L.wl_grad_adj.argtypes = [vp, vp, i64, vp, vp, vp, vp, ci, vp, vp]
+    L.wl_fista_step.argtypes = [vp, vp, i64, vp, vp, vp, cd, cd, cd, vp, ci, vp, vp]
     L.wl_lipschitz.argtypes = [vp, vp, ci, ctypes.c_uint64, dp, vp, vp]
     L.wl_last_error.restype = ctypes.c_char_p
     L.wl_launch_count.restype = ctypes.c_int64
@@ -351,8 +352,12 @@ class Blur:
             pass
 
 
-def grad(plan: Plan, blur: Blur, x, b, out=None, f=None, ws=None, stream=None):
-    """grad f(x) = W* R* (R W x - b); f (optional float64 [batch]) <- 1/2 ||R W x - b||^2."""
+ADJOINTS = {"true": 0, "pinv": 1}  # wl_adj: close the gradient with W* or with W-dagger
+
+
+def grad(plan: Plan, blur: Blur, x, b, out=None, f=None, ws=None, stream=None, adjoint="true"):
+    """grad f(x) = W* R* (R W x - b); f (optional float64 [batch]) <- 1/2 ||R W x - b||^2.
+    adjoint="pinv" closes it with W-dagger instead of W* (the approximation P:113-117 compares)."""
     torch = _torch()
     _require(x, "x", plan.torch_dtype, (plan.p_alloc,))
     _require(b, "b", plan.torch_dtype, (plan.h, plan.w))
@@ -362,7 +367,12 @@ def grad(plan: Plan, blur: Blur, x, b, out=None, f=None, ws=None, stream=None):
     if f is not None:
         _require(f, "f", torch.float64)
     ws = plan._ws(OP_GRAD, B, blur=blur, ws=ws)
-    _check(lib().wl_grad(plan._h, blur._h, B, _ptr(x), _ptr(b), _ptr(out), _ptr(f), _ptr(ws), _stream_ptr(stream)))
+    if adjoint == "true":
+        _check(lib().wl_grad(plan._h, blur._h, B, _ptr(x), _ptr(b), _ptr(out), _ptr(f), _ptr(ws),
+                             _stream_ptr(stream)))
+    else:
+        _check(lib().wl_grad_adj(plan._h, blur._h, B, _ptr(x), _ptr(b), _ptr(out), _ptr(f), ADJOINTS[adjoint],
+                                 _ptr(ws), _stream_ptr(stream)))
     return out
 
 
@@ -391,7 +401,8 @@ def fista_update(plan: Plan, g, x, y, t: float, lam: float, lip: float, stream=N
     return next_t(t)
 
 
-def fista_step(plan: Plan, blur: Blur, b, x, y, t: float, lam: float, lip: float, f=None, ws=None, stream=None):
+def fista_step(plan: Plan, blur: Blur, b, x, y, t: float, lam: float, lip: float, f=None, ws=None, stream=None,
+               adjoint="true"):
     """One FISTA iteration on the GPU (grad f(y) then the fused prox + momentum update); returns t+."""
     _require(b, "b", plan.torch_dtype, (plan.h, plan.w))
     _require(x, "x", plan.torch_dtype, (plan.p_alloc,))
@@ -401,11 +412,12 @@ def fista_step(plan: Plan, blur: Blur, b, x, y, t: float, lam: float, lip: float
         _require(f, "f", _torch().float64)
     ws = plan._ws(OP_FISTA, B, blur=blur, ws=ws)
     _check(lib().wl_fista_step(plan._h, blur._h, B, _ptr(b), _ptr(x), _ptr(y), float(t), float(lam), float(lip),
-                               _ptr(f), _ptr(ws), _stream_ptr(stream)))
+                               _ptr(f), ADJOINTS[adjoint], _ptr(ws), _stream_ptr(stream)))
     return next_t(t)
 
 
-def fista(plan: Plan, blur: Blur, b, lam: float, iters: int, lip: float = None, x0=None, stream=None):
+def fista(plan: Plan, blur: Blur, b, lam: float, iters: int, lip: float = None, x0=None, stream=None,
+          adjoint="true"):
     """FISTA for min_x 1/2 ||R W x - b||^2 + lam ||x||_1 (Eq. (1); P:117 runs 2500 iterations).
     Returns (x, y, t)."""
     torch = _torch()
@@ -417,5 +429,5 @@ def fista(plan: Plan, blur: Blur, b, lam: float, iters: int, lip: float = None, 
     ws = plan._ws(OP_FISTA, B, blur=blur)
     t = 1.0
     for _ in range(int(iters)):
-        t = fista_step(plan, blur, b, x, y, t, lam, lip, ws=ws, stream=stream)
+        t = fista_step(plan, blur, b, x, y, t, lam, lip, ws=ws, stream=stream, adjoint=adjoint)
     return x, y, t

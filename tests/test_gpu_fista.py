@@ -118,3 +118,33 @@ def test_fused_step_equals_grad_then_update(torch, filt, bc, dtype, tol):
     valid = np.zeros(plan.p_alloc, bool)
     valid[plan.to_packed(np.arange(plan.p_alloc)[None].astype(np.float64))[0].astype(np.int64)] = True
     assert np.all(xd.cpu().numpy()[:, ~valid] == 0) and np.all(yd.cpu().numpy()[:, ~valid] == 0)
+
+
+@pytest.mark.parametrize("filt,bc", [("cdf97", "symmetric"), ("db4", "symmetric_edag"), ("haar", "symmetric")])
+@pytest.mark.parametrize("dtype,tol", [("float64", 1e-12), ("float32", 2e-6)])
+def test_pinv_gradient_matches_oracle(torch, filt, bc, dtype, tol):
+    """wl_grad_adj(WL_ADJ_PINV): W-dagger closes the gradient."""
+    h, w, J, B = 66, 50, 3, 2
+    plan = wl.Plan(h, w, J, filt, bc, dtype)
+    blur = wl.Blur(h, w, 15, 3.0, dtype=dtype)
+    rng = np.random.default_rng(8)
+    x = inputs.cast(rng.standard_normal((B, plan.p_valid)), dtype)
+    b = inputs.cast(rng.standard_normal((B, h, w)), dtype)
+    go, fo = O.grad(x.astype(np.float64), b.astype(np.float64), J, filt, bc, adjoint="pinv")
+    f = torch.zeros(B, dtype=torch.float64, device="cuda")
+    g = wl.grad(plan, blur, dev(torch, plan.from_packed(x), dtype), dev(torch, b, dtype), f=f, adjoint="pinv")
+    assert rel(plan.to_packed(g.double().cpu().numpy()), go) <= tol
+    np.testing.assert_allclose(f.cpu().numpy(), fo, rtol=tol)
+
+
+@pytest.mark.parametrize("dtype,tol", [("float64", 1e-11), ("float32", 1e-4)])
+def test_fista_pinv_iterations_match_oracle(torch, dtype, tol):
+    h, w, J, B, K, filt, bc = 40, 36, 3, 1, 10, "cdf97", "symmetric"
+    plan = wl.Plan(h, w, J, filt, bc, dtype)
+    blur = wl.Blur(h, w, 15, 3.0, dtype=dtype)
+    rng = np.random.default_rng(6)
+    b = inputs.cast(O.blur(inputs.blobs(rng, B, h, w, 8)) + 1e-3 * rng.standard_normal((B, h, w)), dtype)
+    x, y, t, _ = O.fista(np.zeros((B, plan.p_valid)), b, J, filt, bc, 2e-3, 1.05, K, adjoint="pinv")
+    xg, yg, tg = wl.fista(plan, blur, dev(torch, b, dtype), 2e-3, K, lip=1.05, adjoint="pinv")
+    assert rel(plan.to_packed(xg.double().cpu().numpy()), x) <= tol
+    assert rel(plan.to_packed(yg.double().cpu().numpy()), y) <= tol

@@ -6,7 +6,11 @@ Pinned by what mathematics fixes, not by the oracle itself:
   * lasso optimality: lambda >= ||(R W)^T b||_inf  =>  the minimiser is 0 and FISTA returns 0;
   * convergence: after many iterations the KKT conditions of min 1/2||RWx-b||^2 + lambda||x||_1 hold,
     checked with the dense matrix (R W) assembled column by column;
-  * momentum sequence t_k: the closed-form recursion t_{k+1} = (1 + sqrt(1 + 4 t_k^2)) / 2.
+  * momentum sequence t_k: the closed-form recursion t_{k+1} = (1 + sqrt(1 + 4 t_k^2)) / 2;
+  * the W-dagger-closed gradient: equal to the true gradient for orthogonal filters
+    under zero / periodic BC (W*_zpd = W-dagger_zpd for orthogonal wavelets), different
+    for biorthogonal CDF 9/7 under symmetric BC, and equal to the dense A R^T (R W x - b) with A
+    the assembled analysis matrix.
 """
 import numpy as np
 import pytest
@@ -76,3 +80,34 @@ def test_momentum_sequence(oracle_lib):
         assert t_new == pytest.approx((1 + np.sqrt(1 + 4 * t * t)) / 2)
         assert t_new > t and t_new >= (k + 1) / 2
         t = t_new
+
+
+@pytest.mark.parametrize("filt", ["haar", "db2", "db4"])
+@pytest.mark.parametrize("bc", ["zero", "periodic"])
+def test_pinv_gradient_is_true_gradient_for_orthogonal(oracle_lib, filt, bc):
+    O = oracle_lib
+    h, w, j = 16, 24, 2
+    p = O.layout(h, w, j, filt, bc).p
+    rng = np.random.default_rng(3)
+    x, b = rng.standard_normal((2, p)), rng.standard_normal((2, h, w))
+    gt, ft = O.grad(x, b, j, filt, bc)
+    gp, fp = O.grad(x, b, j, filt, bc, adjoint="pinv")
+    np.testing.assert_allclose(gp, gt, rtol=0, atol=1e-12 * np.abs(gt).max())
+    np.testing.assert_array_equal(fp, ft)
+
+
+def test_pinv_gradient_dense_and_differs_for_biorthogonal(oracle_lib):
+    O = oracle_lib
+    h, w, j, filt, bc = 14, 12, 1, "cdf97", "symmetric"
+    p = O.layout(h, w, j, filt, bc).p
+    E = np.eye(h * w).reshape(h * w, h, w)
+    A = O.analyze(E, j, filt, bc).T                                            # (p, hw): column k = W-dagger e_k
+    Wm = O.synthesize(np.eye(p), h, w, j, filt, bc).reshape(p, h * w).T        # (hw, p)
+    Rm = O.blur(E).reshape(h * w, h * w).T                                     # (hw, hw)
+    rng = np.random.default_rng(4)
+    x, b = rng.standard_normal(p), rng.standard_normal((h, w))
+    r = Rm @ (Wm @ x) - b.ravel()
+    gp, _ = O.grad(x[None], b[None], j, filt, bc, adjoint="pinv")
+    np.testing.assert_allclose(gp[0], A @ (Rm.T @ r), atol=1e-11 * np.abs(gp).max())
+    gt, _ = O.grad(x[None], b[None], j, filt, bc)
+    assert np.linalg.norm(gp - gt) > 1e-3 * np.linalg.norm(gt)
