@@ -118,6 +118,33 @@ def chart(h: int, w: int) -> np.ndarray:
     return img
 
 
+# Example 2: two channels, true lengths K = 894, N = 1717, guessed K_est = 844, N_est = 1767,
+# noise std 0.005; lambda_TV = 0.01, delta = 0.1.  The Rideout simulation is missing: spike trains stand in.
+BCE = dict(channels=2, K=894, N=1717, K_est=844, N_est=1767, noise=0.005, lam_tv=0.01, delta=0.1)
+
+
+def spikes(g: np.random.Generator, shape, density: float) -> np.ndarray:
+    """Sparse spike train(s): Bernoulli(density) support x N(0, 1) amplitudes (fp64)."""
+    mask = g.random(shape) < density
+    return np.where(mask, g.standard_normal(shape), 0.0)
+
+
+def bce_problem(seed: int, problems: int, channels: int, K: int, N: int, K_est: int, N_est: int,
+                noise_std: float, density: float = 0.02):
+    """One observed multi-channel record and `problems` random starts (the paper initialises h_i
+    and s with N(0, 1) numbers).  Draw order: true h [C, K], true s [N], noise [C, K+N-1],
+    then h0 [P, C, K_est], s0 [P, N_est].  Returns fp64 (h_true, s_true, noise, h0, s0); the observation
+    x = h_true * s_true + noise is formed by the caller's own convolution."""
+    assert K + N == K_est + N_est, "the guessed lengths must keep the observed length K+N-1"
+    g = np.random.Generator(np.random.PCG64(seed))
+    h_true = spikes(g, (channels, K), density)
+    s_true = spikes(g, (N,), density)
+    nz = noise_std * g.standard_normal((channels, K + N - 1))
+    h0 = g.standard_normal((problems, channels, K_est))
+    s0 = g.standard_normal((problems, N_est))
+    return h_true, s_true, nz, h0, s0
+
+
 def noise(g: np.random.Generator, batch: int, h: int, w: int) -> np.ndarray:
     return NOISE_STD * g.standard_normal((batch, h, w))
 
