@@ -235,6 +235,37 @@ WL_API wl_status wl_fista_step(const wl_plan *plan, const wl_blur_plan *blur, in
 WL_API wl_status wl_lipschitz(const wl_plan *plan, const wl_blur_plan *blur, int iters, uint64_t seed,
                        double *lip_host, void *ws, void *stream);
 
+/* ------------------------------------------------- Example 2: blind channel estimation */
+
+/* PAPER.md §"Example 2: Blind Channel Estimation".  Real signals,
+ * zero-padded boundaries.  All arrays are contiguous device arrays of `dtype`, batch-major; the
+ * caller owns them; outputs must not overlap inputs (WL_EINVAL).  Sizes are limited by one CTA's
+ * shared memory (WL_ESIZE names the need): the paper's K_est = 844, N_est = 1767 with two channels
+ * use 49 KB (fp32) / 98 KB (fp64).  Element alignment only.  Stream-ordered, asynchronous. */
+
+/* x_est = h * s, the "full" convolution x[m] = sum_k h[k] s[m-k], m < K+N-1.
+ * h [batch, K], s [batch, N] -> x [batch, K+N-1]. */
+WL_API wl_status wl_conv_full(wl_dtype dtype, int64_t batch, int64_t K, int64_t N, const void *h, const void *s,
+                       void *x, void *stream);
+/* S* r: the "valid" cross-correlation gh[n] = sum_{k<N} s[k] r[k+n], n < K (MATLAB
+ * conv(r, conj(s(end:-1:1)), 'valid')).  s [batch, N], r [batch, K+N-1] -> gh [batch, K]. */
+WL_API wl_status wl_conv_adjoint_h(wl_dtype dtype, int64_t batch, int64_t K, int64_t N, const void *s, const void *r,
+                            void *gh, void *stream);
+/* H* r: gs[k] = sum_{n<K} h[n] r[k+n], k < N.  h [batch, K], r [batch, K+N-1] -> gs [batch, N]. */
+WL_API wl_status wl_conv_adjoint_s(wl_dtype dtype, int64_t batch, int64_t K, int64_t N, const void *h, const void *r,
+                            void *gs, void *stream);
+/* Gradient of the smooth part of Eq. (6), fused, for `problems` independent problems
+ * of `channels` channels sharing one source:
+ *     F = sum_i ||h_i * s - x_i||^2 + (lam_tv / delta) sum_i L_delta(D h_i)     (no 1/2: Eq. (6))
+ *     gh_i = 2 S* r_i + (lam_tv / delta) D^T L_delta'(D h_i),  gs = 2 sum_i H_i* r_i,  r_i = h_i * s - x_i
+ * with (D h)_j = h_{j+1} - h_j and the Huber function L_delta.
+ * h [problems, channels, K], s [problems, N], x [problems, channels, K+N-1] (x_shared != 0: one
+ * [channels, K+N-1] observation for every problem, e.g. random restarts) -> gh like h, gs like s,
+ * f_dev (nullable) double[problems] <- F.  delta > 0, lam_tv >= 0. */
+WL_API wl_status wl_bce_grad(wl_dtype dtype, int64_t problems, int channels, int64_t K, int64_t N, const void *h,
+                      const void *s, const void *x, int x_shared, double lam_tv, double delta, void *gh,
+                      void *gs, double *f_dev, void *stream);
+
 /* ---------------------------------------------------------------- misc */
 
 WL_API const char *wl_last_error(void); /* thread-local; never NULL */

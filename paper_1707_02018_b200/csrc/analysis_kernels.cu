@@ -359,8 +359,9 @@ __global__ void __launch_bounds__(ACfg<T, L>::NT, sizeof(T) == 4 ? 768 / ACfg<T,
       __syncthreads();  // (3) history readers done
       // carry history rows [GI, GI+L-2) to [0, L-2) in both sets
       constexpr int CPR = TQ / VEC;
+      constexpr int HC = (L - 2) * CPR > 0 ? (L - 2) * CPR : 1;  // (Haar carries nothing)
       for (int idx = tid; idx < 2 * (L - 2) * CPR; idx += C::NT) {
-        const int set = idx / ((L - 2) * CPR), rem = idx - set * (L - 2) * CPR;
+        const int set = idx / HC, rem = idx - set * HC;
         const int r = rem / CPR, c = rem - r * CPR;
         T *hb = hist + set * C::HR * C::HP;
         *reinterpret_cast<Vt *>(hb + r * C::HP + c * VEC) = *reinterpret_cast<const Vt *>(hb + (r + GI) * C::HP + c * VEC);

@@ -78,6 +78,8 @@ wl_status check_dev(const void *p, const char *name, size_t align = 16) {
   return WL_OK;
 }
 
+constexpr size_t kMaxSmemOptin = 227 * 1024;  // sm_100a opt-in dynamic shared memory per CTA
+
 bool overlap(const void *a, size_t na, const void *b, size_t nb) {
   auto x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
   return na && nb && x < y + nb && y < x + na;
@@ -711,6 +713,114 @@ wl_status wl_lipschitz(const wl_plan *p, const wl_blur_plan *bl, int iters, uint
     if (e != cudaSuccess) return cuda_fail(e, "wl_lipschitz copy");
   }
   *lip_host = est;
+  return ok();
+}
+
+// ------------------------------------------------------------- Example 2
+static wl_status bce_sizes(const char *fn, wl_dtype dtype, int64_t batch, int64_t K, int64_t N) {
+  if (dtype != WL_F32 && dtype != WL_F64) return fail(WL_EDTYPE, "%s: dtype=%d", fn, (int)dtype);
+  if (batch < 0) return fail(WL_EINVAL, "%s: batch=%lld < 0", fn, (long long)batch);
+  if (K < 1 || N < 1) return fail(WL_ESIZE, "%s: K=%lld and N=%lld must be >= 1", fn, (long long)K, (long long)N);
+  if (K + N > (int64_t)1 << 24) return fail(WL_ESIZE, "%s: K+N=%lld too long", fn, (long long)(K + N));
+  return WL_OK;
+}
+
+static wl_status xcorr_call(const char *fn, wl_dtype dtype, int64_t batch, const void *a, int64_t a_len, int a_rev,
+                            const void *b, int64_t b_len, int64_t b_off, void *out, int64_t n_out, void *stream) {
+  const size_t es = dtype == WL_F64 ? 8 : 4;
+  const size_t smem = xcorr_smem_bytes(dtype, (int)a_len, (int)n_out);
+  if (smem > kMaxSmemOptin)
+    return fail(WL_ESIZE, "%s: operands need %zu bytes of shared memory (max %zu)", fn, smem, kMaxSmemOptin);
+  wl_status st;
+  if ((st = check_dev(a, "a", es)) || (st = check_dev(b, "b", es)) || (st = check_dev(out, "out", es))) return st;
+  const size_t ob = (size_t)batch * n_out * es;
+  if (overlap(a, (size_t)batch * a_len * es, out, ob) || overlap(b, (size_t)batch * b_len * es, out, ob))
+    return fail(WL_EINVAL, "%s: out overlaps an input", fn);
+  XcorrArgs x;
+  x.a = a;
+  x.a_bstride = a_len;
+  x.ta = (int)a_len;
+  x.a_rev = a_rev;
+  x.b = b;
+  x.b_bstride = b_len;
+  x.lb = (int)b_len;
+  x.b_off = (int)b_off;
+  x.out = out;
+  x.out_bstride = n_out;
+  x.n_out = (int)n_out;
+  x.batch = batch;
+  cudaError_t e = launch_xcorr(dtype, x, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, fn);
+  return ok();
+}
+
+wl_status wl_conv_full(wl_dtype dtype, int64_t batch, int64_t K, int64_t N, const void *h, const void *s, void *x,
+                       void *stream) {
+  wl_status st = bce_sizes("wl_conv_full", dtype, batch, K, N);
+  if (st) return st;
+  if (batch == 0) return ok();
+  // x[m] = sum_k h[k] s[m-k] = sum_j h[K-1-j] s_pad[m+j], s_pad = s shifted by K-1
+  return xcorr_call("wl_conv_full", dtype, batch, h, K, 1, s, N, K - 1, x, K + N - 1, stream);
+}
+
+wl_status wl_conv_adjoint_h(wl_dtype dtype, int64_t batch, int64_t K, int64_t N, const void *s, const void *r,
+                            void *gh, void *stream) {
+  wl_status st = bce_sizes("wl_conv_adjoint_h", dtype, batch, K, N);
+  if (st) return st;
+  if (batch == 0) return ok();
+  return xcorr_call("wl_conv_adjoint_h", dtype, batch, s, N, 0, r, K + N - 1, 0, gh, K, stream);
+}
+
+wl_status wl_conv_adjoint_s(wl_dtype dtype, int64_t batch, int64_t K, int64_t N, const void *h, const void *r,
+                            void *gs, void *stream) {
+  wl_status st = bce_sizes("wl_conv_adjoint_s", dtype, batch, K, N);
+  if (st) return st;
+  if (batch == 0) return ok();
+  return xcorr_call("wl_conv_adjoint_s", dtype, batch, h, K, 0, r, K + N - 1, 0, gs, N, stream);
+}
+
+wl_status wl_bce_grad(wl_dtype dtype, int64_t problems, int channels, int64_t K, int64_t N, const void *h,
+                      const void *s, const void *x, int x_shared, double lam_tv, double delta, void *gh, void *gs,
+                      double *f_dev, void *stream) {
+  wl_status st = bce_sizes("wl_bce_grad", dtype, problems, K, N);
+  if (st) return st;
+  if (channels < 1 || channels > 64) return fail(WL_EINVAL, "wl_bce_grad: channels=%d not in [1, 64]", channels);
+  if (!(delta > 0) || !std::isfinite(delta)) return fail(WL_EINVAL, "wl_bce_grad: delta=%g must be > 0", delta);
+  if (!(lam_tv >= 0) || !std::isfinite(lam_tv)) return fail(WL_EINVAL, "wl_bce_grad: lam_tv=%g must be >= 0", lam_tv);
+  if (problems == 0) return ok();
+  BceArgs a;
+  a.h = h;
+  a.s = s;
+  a.x = x;
+  a.x_shared = x_shared ? 1 : 0;
+  a.gh = gh;
+  a.gs = gs;
+  a.f = f_dev;
+  a.C = channels;
+  a.K = (int)K;
+  a.N = (int)N;
+  a.problems = problems;
+  a.lam_tv = lam_tv;
+  a.delta = delta;
+  const size_t es = dtype == WL_F64 ? 8 : 4;
+  const size_t smem = bce_smem_bytes(dtype, a);
+  if (smem > kMaxSmemOptin)
+    return fail(WL_ESIZE, "wl_bce_grad: C=%d K=%lld N=%lld need %zu bytes of shared memory (max %zu)", channels,
+                (long long)K, (long long)N, smem, kMaxSmemOptin);
+  if ((st = check_dev(h, "h", es)) || (st = check_dev(s, "s", es)) || (st = check_dev(x, "x", es)) ||
+      (st = check_dev(gh, "gh", es)) || (st = check_dev(gs, "gs", es)))
+    return st;
+  if (f_dev && (st = check_dev(f_dev, "f_dev", 8))) return st;
+  const size_t hb = (size_t)problems * channels * K * es, sb = (size_t)problems * N * es;
+  const size_t xb = (size_t)(x_shared ? 1 : problems) * channels * (K + N - 1) * es;
+  const void *ins[3] = {h, s, x};
+  const size_t inb[3] = {hb, sb, xb};
+  for (int i = 0; i < 3; i++)
+    if (overlap(ins[i], inb[i], gh, hb) || overlap(ins[i], inb[i], gs, sb))
+      return fail(WL_EINVAL, "wl_bce_grad: an output overlaps an input");
+  if (overlap(gh, hb, gs, sb)) return fail(WL_EINVAL, "wl_bce_grad: gh and gs overlap");
+  cudaError_t e = launch_bce_grad(dtype, a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "wl_bce_grad launch");
   return ok();
 }
 

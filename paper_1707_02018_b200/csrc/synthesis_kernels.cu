@@ -302,9 +302,10 @@ __global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 768 / SCfg<T,
       }
       __syncthreads();  // (3) V history readers done
       // carry V rows [G, G+H-1) to the head of the history
+      constexpr int HC = (H - 1) * (C::TW / VEC) > 0 ? (H - 1) * (C::TW / VEC) : 1;  // (Haar carries nothing)
       for (int idx = tid; idx < 2 * (H - 1) * (C::TW / VEC); idx += C::NT) {
-        const int half = idx / ((H - 1) * (C::TW / VEC));
-        const int rem = idx - half * (H - 1) * (C::TW / VEC);
+        const int half = idx / HC;
+        const int rem = idx - half * HC;
         const int r = rem / (C::TW / VEC), c = rem - r * (C::TW / VEC);
         T *hb = half ? vh : vl;
         *reinterpret_cast<Vt *>(hb + r * C::TWP + c * VEC) = *reinterpret_cast<const Vt *>(hb + (r + G) * C::TWP + c * VEC);

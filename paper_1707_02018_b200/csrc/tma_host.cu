@@ -67,27 +67,31 @@ bool encode_tmap_3d(void *map, int elem_bytes, const void *base, uint64_t d0, ui
 cudaError_t kernel_resident(const void *kern, int nt, size_t smem, long long *resident) {
   static std::mutex mu;
   static std::map<std::tuple<const void *, int, int, size_t>, long long> cache;
+  static std::map<std::pair<const void *, int>, size_t> opted;  // largest smem opted in per (kernel, device)
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   const auto key = std::make_tuple(kern, dev, nt, smem);
-  {
-    std::lock_guard<std::mutex> g(mu);
-    auto it = cache.find(key);
-    if (it != cache.end()) {
-      *resident = it->second;
-      return cudaSuccess;
-    }
+  std::lock_guard<std::mutex> g(mu);
+  // the opt-in only ever grows: a later, smaller request must not lower it below a size
+  // another (cached) launch of the same kernel relies on
+  size_t &cur = opted[std::make_pair(kern, dev)];
+  if (smem > cur) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cur = smem;
   }
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *resident = it->second;
+    return cudaSuccess;
+  }
   int sms = 0, occ = 0;
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, smem);
   if (e != cudaSuccess) return e;
   const long long r = (long long)sms * (occ > 0 ? occ : 1);
-  std::lock_guard<std::mutex> g(mu);
   cache[key] = r;
   *resident = r;
   return cudaSuccess;

@@ -84,6 +84,35 @@ cudaError_t launch_blur(int dtype, const BlurArgs &a, cudaStream_t s);
 cudaError_t launch_blur_residual(int dtype, const BlurArgs &a, cudaStream_t s);
 cudaError_t launch_zero(void *ptr, size_t bytes, cudaStream_t s);
 // FISTA pieces (fista_kernels.cu); n = elements per call (batch * p_alloc for the update)
+// Example 2: batched valid cross-correlation out_b[i] = sum_{j<ta} a_b[j] b_b[i+j]
+// with a_b[j] = a[ta-1-j] if a_rev, and b_b[i] = b[i - b_off] on [b_off, b_off + lb), else 0.
+struct XcorrArgs {
+  const void *a;
+  int64_t a_bstride;
+  int ta, a_rev;
+  const void *b;
+  int64_t b_bstride;
+  int lb, b_off;
+  void *out;
+  int64_t out_bstride;
+  int n_out;
+  int64_t batch;
+};
+// Fused gradient of Eq. (6) for `problems` independent (h [C][K], s [N]) pairs.
+struct BceArgs {
+  const void *h, *s, *x;
+  int x_shared;
+  void *gh, *gs;
+  double *f;
+  int C, K, N;
+  int64_t problems;
+  double lam_tv, delta;
+};
+size_t xcorr_smem_bytes(int dtype, int ta, int n_out);
+size_t bce_smem_bytes(int dtype, const BceArgs &a);
+cudaError_t launch_xcorr(int dtype, const XcorrArgs &x, cudaStream_t s);
+cudaError_t launch_bce_grad(int dtype, const BceArgs &a, cudaStream_t s);
+
 cudaError_t launch_fista_update(int dtype, const void *g, void *x, void *y, long long n, double t, double lambda,
                                 double lip, cudaStream_t s);
 cudaError_t launch_dot(int dtype, const void *a, const void *b, long long n, int batch, double *out, cudaStream_t s);

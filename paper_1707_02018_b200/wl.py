@@ -47,7 +47,8 @@ class _PlanInfo(ctypes.Structure):
 EXPORTS = ("wl_plan_create", "wl_plan_destroy", "wl_plan_query", "wl_plan_filters", "wl_workspace_bytes",
            "wl_synthesize", "wl_adjoint", "wl_analyze", "wl_analyze_adjoint", "wl_blur_create", "wl_blur_create_gaussian",
            "wl_blur_destroy", "wl_blur_taps", "wl_blur", "wl_blur_adjoint", "wl_blur_residual_adjoint",
-           "wl_grad", "wl_grad_adj", "wl_fista_update", "wl_fista_step", "wl_lipschitz", "wl_last_error", "wl_launch_count",
+           "wl_grad", "wl_grad_adj", "wl_fista_update", "wl_fista_step", "wl_lipschitz", "wl_conv_full", "wl_conv_adjoint_h",
+           "wl_conv_adjoint_s", "wl_bce_grad", "wl_last_error", "wl_launch_count",
            "wl_version")
 
 _lib = None
@@ -89,6 +90,9 @@ def lib():
     L.wl_grad_adj.argtypes = [vp, vp, i64, vp, vp, vp, vp, ci, vp, vp]
     L.wl_fista_step.argtypes = [vp, vp, i64, vp, vp, vp, cd, cd, cd, vp, ci, vp, vp]
     L.wl_lipschitz.argtypes = [vp, vp, ci, ctypes.c_uint64, dp, vp, vp]
+    for fn in ("wl_conv_full", "wl_conv_adjoint_h", "wl_conv_adjoint_s"):
+        getattr(L, fn).argtypes = [ci, i64, i64, i64, vp, vp, vp, vp]
+    L.wl_bce_grad.argtypes = [ci, i64, ci, i64, i64, vp, vp, vp, ci, cd, cd, vp, vp, vp, vp]
     L.wl_last_error.restype = ctypes.c_char_p
     L.wl_launch_count.restype = ctypes.c_int64
     L.wl_version.restype = ctypes.c_char_p
@@ -431,3 +435,95 @@ def fista(plan: Plan, blur: Blur, b, lam: float, iters: int, lip: float = None, 
     for _ in range(int(iters)):
         t = fista_step(plan, blur, b, x, y, t, lam, lip, ws=ws, stream=stream, adjoint=adjoint)
     return x, y, t
+
+
+# ------------------------------------------------------------------ Example 2
+def _dtype_of(t):
+    return _dtype_code(t.dtype)
+
+
+def _check_1d(t, name, n, dtype=None):
+    """Metadata checks of a [..., n] signal tensor; returns the flattened batch size."""
+    torch = _torch()
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if t.shape[-1] != n:
+        raise ValueError(f"{name} has last dim {t.shape[-1]}, expected {n}")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name} has dtype {t.dtype}, expected {dtype}")
+    return int(np.prod(t.shape[:-1])) if t.dim() > 1 else 1
+
+
+def conv_full(h, s, out=None, stream=None):
+    """x_est = h * s, full convolution: h [..., K], s [..., N] -> [..., K+N-1]."""
+    K, N = h.shape[-1], s.shape[-1]
+    B = _check_1d(h, "h", K)
+    if _check_1d(s, "s", N, h.dtype) != B:
+        raise ValueError("h and s must have the same batch shape")
+    if out is None:
+        out = _torch().empty(h.shape[:-1] + (K + N - 1,), dtype=h.dtype, device=h.device)
+    _check_1d(out, "out", K + N - 1, h.dtype)
+    _check(lib().wl_conv_full(_dtype_of(h), B, K, N, _ptr(h), _ptr(s), _ptr(out), _stream_ptr(stream)))
+    return out
+
+
+def conv_adjoint_h(s, r, K: int, out=None, stream=None):
+    """S* r = valid cross-correlation of r with s: s [..., N], r [..., K+N-1] -> [..., K]."""
+    N = s.shape[-1]
+    B = _check_1d(s, "s", N)
+    if _check_1d(r, "r", K + N - 1, s.dtype) != B:
+        raise ValueError("s and r must have the same batch shape")
+    if out is None:
+        out = _torch().empty(s.shape[:-1] + (K,), dtype=s.dtype, device=s.device)
+    _check_1d(out, "out", K, s.dtype)
+    _check(lib().wl_conv_adjoint_h(_dtype_of(s), B, K, N, _ptr(s), _ptr(r), _ptr(out), _stream_ptr(stream)))
+    return out
+
+
+def conv_adjoint_s(h, r, N: int, out=None, stream=None):
+    """H* r (P:246): h [..., K], r [..., K+N-1] -> [..., N]."""
+    K = h.shape[-1]
+    B = _check_1d(h, "h", K)
+    if _check_1d(r, "r", K + N - 1, h.dtype) != B:
+        raise ValueError("h and r must have the same batch shape")
+    if out is None:
+        out = _torch().empty(h.shape[:-1] + (N,), dtype=h.dtype, device=h.device)
+    _check_1d(out, "out", N, h.dtype)
+    _check(lib().wl_conv_adjoint_s(_dtype_of(h), B, K, N, _ptr(h), _ptr(r), _ptr(out), _stream_ptr(stream)))
+    return out
+
+
+def bce_grad(h, s, x, lam_tv: float = 0.01, delta: float = 0.1, gh=None, gs=None, f=None, stream=None):
+    """Gradient of the smooth part of Eq. (6), fused on the GPU.
+
+    h [P, C, K], s [P, N], x [P, C, K+N-1] or [C, K+N-1] (one observation shared by all P problems)
+    -> (gh [P, C, K], gs [P, N]); f (optional float64 [P]) <- the smooth objective.
+    """
+    torch = _torch()
+    if h.dim() != 3 or s.dim() != 2:
+        raise ValueError("h must be [P, C, K] and s [P, N]")
+    P, C, K = h.shape
+    N = s.shape[-1]
+    _check_1d(h, "h", K)
+    if _check_1d(s, "s", N, h.dtype) != P:
+        raise ValueError("s must be [P, N] with the P of h")
+    _check_1d(x, "x", K + N - 1, h.dtype)
+    if x.dim() == 2 and tuple(x.shape) == (C, K + N - 1):
+        shared = 1
+    elif x.dim() == 3 and tuple(x.shape) == (P, C, K + N - 1):
+        shared = 0
+    else:
+        raise ValueError(f"x must be [P, C, K+N-1] or [C, K+N-1], got {tuple(x.shape)}")
+    gh = torch.empty_like(h) if gh is None else gh
+    gs = torch.empty_like(s) if gs is None else gs
+    _check_1d(gh, "gh", K, h.dtype)
+    _check_1d(gs, "gs", N, h.dtype)
+    if f is not None:
+        _require(f, "f", torch.float64)
+    _check(lib().wl_bce_grad(_dtype_of(h), P, C, K, N, _ptr(h), _ptr(s), _ptr(x), shared, float(lam_tv),
+                             float(delta), _ptr(gh), _ptr(gs), _ptr(f), _stream_ptr(stream)))
+    return gh, gs
