@@ -30,6 +30,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "W* and ∇f GB/s and % HBM roofline at 4096² fp32; gradient evals/sec"
 FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback if MEASURED_PEAKS.json is absent
+FFMA_PEAK_TFLOPS = 74.4     # 148 SMs x 128 FP32 lanes x 2 flop x 1.965 GHz (ALU ceiling)
 
 
 def measured_peaks():
@@ -282,6 +283,26 @@ def run_wl(args):
              "config": "cfg5, lambda 1e-3, L 1"}
     del xf, yf, wsf
 
+    # ---- Example 2: fused Eq. (6) gradient, paper sizes, 4096 random starts
+    bc = inputs.BCE
+    P_bce, C_b, K_b, N_b = 4096, bc["channels"], bc["K_est"], bc["N_est"]
+    _, _, _, h0, s0 = inputs.bce_problem(7, P_bce, C_b, bc["K"], bc["N"], K_b, N_b, bc["noise"])
+    hb_ = torch.from_numpy(h0.astype(np.float32)).to(dev)
+    sb_ = torch.from_numpy(s0.astype(np.float32)).to(dev)
+    xb_ = torch.randn(C_b, K_b + N_b - 1, device=dev, generator=torch.Generator(dev).manual_seed(7))
+    ghb, gsb = torch.empty_like(hb_), torch.empty_like(sb_)
+    fb_ = torch.empty(P_bce, dtype=torch.float64, device=dev)
+    t_b = time_calls(torch, lambda: wl.bce_grad(hb_, sb_, xb_, bc["lam_tv"], bc["delta"], gh=ghb, gs=gsb, f=fb_),
+                     max(args.steps, 10))
+    flops_b = 2.0 * 3 * C_b * K_b * N_b * P_bce
+    tf_b = flops_b / (t_b * 1e-3) / 1e12
+    bce = {"workload": f"Eq. (6) gradient, {P_bce} random starts x {C_b} channels, K={K_b}, N={N_b}, fp32",
+           "ms": t_b, "grads_per_s": ws * P_bce / (t_b * 1e-3),
+           "roofline": {"bound": "alu", "achieved": tf_b, "peak": FFMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                        "frac": tf_b / FFMA_PEAK_TFLOPS, "flops_per_launch": flops_b,
+                        "peak_source": "148 SMs x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md §6)"}}
+    del hb_, sb_, xb_, ghb, gsb, fb_
+
     # ---- end to end through the public API with host buffers (pinned), copies inside
     xh = x.cpu().pin_memory()
     bh = b.cpu().pin_memory()
@@ -327,7 +348,7 @@ def run_wl(args):
                            "bytes_per_step_per_gpu": nbytes},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(), "grad_evals_per_s": ws / (ms * 1e-3), "images_per_s": ws * B / (ms * 1e-3),
-                "grad_frac_of_hbm_roofline": value / ws / hbm_peak, "wstar_cfg4": wstar, "fista_cfg5": fista, "kernels": kernels}
+                "grad_frac_of_hbm_roofline": value / ws / hbm_peak, "wstar_cfg4": wstar, "fista_cfg5": fista, "bce": bce, "kernels": kernels}
         print(json.dumps(line))
     if ws > 1:
         import torch.distributed as dist
