@@ -1,0 +1,42 @@
+#!/usr/bin/env python
+"""Headline metrics and warp-stall breakdown of the kernel(s) in an ncu report.
+
+  python tools/ncu_stalls.py gpurun_out/prof.ncu-rep
+"""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = ["gpu__time_duration.sum", "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
+        "launch__occupancy_limit_shared_mem", "launch__occupancy_limit_registers",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "smsp__inst_executed.sum", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"]
+
+
+def main():
+    txt = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    hdr, units = rows[0], rows[1]
+    for v in rows[2:]:
+        print("==", v[hdr.index("Kernel Name")][:100])
+        for k in KEYS:
+            if k in hdr:
+                print(f"  {k:70s} {units[hdr.index(k)]:>8s} {v[hdr.index(k)]}")
+        st = []
+        for i, k in enumerate(hdr):
+            if k.startswith("smsp__average_warp_latency_issue_stalled_") or (
+                    k.startswith("smsp__warp_issue_stalled_") and k.endswith("_per_warp_active.pct")):
+                try:
+                    st.append((float(v[i]), k))
+                except ValueError:
+                    pass
+        for val, k in sorted(st, reverse=True)[:12]:
+            print(f"  {k:70s} {val:.2f}")
+
+
+if __name__ == "__main__":
+    main()
