@@ -216,7 +216,12 @@ def run_wl(args):
     g = torch.empty_like(x)
     f = torch.zeros(B, dtype=torch.float64, device=dev)
     wsb = plan._ws(wl.OP_GRAD, B, blur=blur)
-    step = lambda: wl.grad(plan, blur, x, b, out=g, f=f, ws=wsb)  # noqa: E731
+    step_eager = lambda: wl.grad(plan, blur, x, b, out=g, f=f, ws=wsb)  # noqa: E731
+    # the step runs as a CUDA graph of the library's launches (one graph launch per step; the
+    # same kernels, arguments and work as the eager call) unless --eager
+    graph = None if args.eager else wl.Graph(step_eager)
+    step = step_eager if graph is None else graph.replay
+    per_step = (graph.launches if graph is not None else None)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -232,9 +237,10 @@ def run_wl(args):
             step()
         e1.record(s)
         torch.cuda.synchronize()
-    launches = wl.launch_count() - launches0
+    launches = wl.launch_count() - launches0 if graph is None else per_step * args.steps
     barrier(ws)
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, ws)
+    ms_eager = ms if graph is None else max_over_ranks(time_calls(torch, step_eager, max(args.steps, 5)), ws)
     nbytes = grad_bytes(B, N, plan.p_valid, es)
     value = ws * nbytes / (ms * 1e-3) / 1e9
 
@@ -345,9 +351,11 @@ def run_wl(args):
                            "global_batch": B * ws, "h": c.h, "w": c.w, "levels": c.levels, "filter": c.filt,
                            "bc": c.bc, "parallelism": f"replicas x{ws}",
                            "l2": "inputs larger than L2 (x + b = 538 MB per step per GPU), no flush",
+                           "launch": "each step = one replay of a CUDA graph of the wl_grad launches (--eager: direct calls)",
                            "bytes_per_step_per_gpu": nbytes},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clk.summary(), "grad_evals_per_s": ws / (ms * 1e-3), "images_per_s": ws * B / (ms * 1e-3),
+                "clocks": clk.summary(), "step_launch": "eager" if graph is None else "cuda_graph",
+                "ms_per_step_eager": ms_eager, "grad_evals_per_s": ws / (ms * 1e-3), "images_per_s": ws * B / (ms * 1e-3),
                 "grad_frac_of_hbm_roofline": value / ws / hbm_peak, "wstar_cfg4": wstar, "fista_cfg5": fista, "bce": bce, "kernels": kernels}
         print(json.dumps(line))
     if ws > 1:
@@ -363,6 +371,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="wl", choices=["wl", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="launch the timed step eagerly instead of as a CUDA graph")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

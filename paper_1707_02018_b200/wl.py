@@ -380,6 +380,30 @@ def grad(plan: Plan, blur: Blur, x, b, out=None, f=None, ws=None, stream=None, a
     return out
 
 
+class Graph:
+    """A CUDA graph of a fixed sequence of libwl calls on fixed buffers (captured once with
+    torch.cuda.graph; every call is stream-ordered and allocation-free, so it is capturable).
+    replay() re-runs every kernel with the captured arguments: the launch sequence of one
+    wl_grad (11 kernels at cfg5) then costs one graph launch instead of 11 host launches."""
+
+    def __init__(self, fn, warmup: int = 1):
+        torch = _torch()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                fn()
+        torch.cuda.current_stream().wait_stream(s)
+        n0 = launch_count()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            fn()
+        self.launches = launch_count() - n0  # libwl kernels per replay
+
+    def replay(self):
+        self.graph.replay()
+
+
 # ------------------------------------------------------------------ FISTA (SURVEY §8(f) NEXT #1)
 def next_t(t: float) -> float:
     """FISTA momentum recursion t_{k+1} = (1 + sqrt(1 + 4 t_k^2)) / 2 (host scalar)."""
