@@ -284,8 +284,12 @@ def run_wl(args):
     # ---- one FISTA iteration at cfg5 (grad f(y) + fused prox/momentum update)
     xf, yf = torch.zeros_like(x), x.clone()
     wsf = plan._ws(wl.OP_FISTA, B, blur=blur)
-    tf = time_calls(torch, lambda: wl.fista_step(plan, blur, b, xf, yf, 2.0, 1e-3, 1.0, ws=wsf), reps)
+    t_dev = torch.full((1,), 2.0, dtype=torch.float64, device=dev)
+    f_step = lambda: wl.fista_step(plan, blur, b, xf, yf, t_dev, 1e-3, 1.0, ws=wsf)  # noqa: E731
+    tf_eager = time_calls(torch, f_step, reps)
+    tf = time_calls(torch, wl.Graph(f_step).replay, reps)
     fista = {"ms_per_iter": tf, "iters_per_s": ws / (tf * 1e-3), "update_overhead_ms": tf - ms,
+             "ms_per_iter_eager": tf_eager, "launch": "cuda_graph (device-resident t)",
              "config": "cfg5, lambda 1e-3, L 1"}
     del xf, yf, wsf
 

@@ -227,6 +227,13 @@ WL_API wl_status wl_fista_update(const wl_plan *plan, int64_t batch, const void 
 WL_API wl_status wl_fista_step(const wl_plan *plan, const wl_blur_plan *blur, int64_t batch, const void *b, void *x,
                         void *y, double t, double lambda, double lip, double *f_dev, wl_adj adj, void *ws,
                         void *stream);
+/* wl_fista_step with the momentum scalar t resident on the device: t_dev (double, device) holds
+ * t_k on entry and t_{k+1} on exit (advanced by a one-thread kernel after the update).  Every
+ * argument of the launch sequence is then the same from one iteration to the next, so a CUDA
+ * graph of one call replays the whole FISTA loop. */
+WL_API wl_status wl_fista_step_dev(const wl_plan *plan, const wl_blur_plan *blur, int64_t batch, const void *b,
+                            void *x, void *y, double *t_dev, double lambda, double lip, double *f_dev, wl_adj adj,
+                            void *ws, void *stream);
 /* Power iteration for lip = lambda_max(W* R* R W): v_0 = a seeded uniform(-1, 1)
  * vector, v <- G v with G v = grad f(v) at b = 0, estimate <v, G v> / <v, v> of the last step
  * (a lower bound that increases to lambda_max).  Blocking: synchronises `stream` every iteration

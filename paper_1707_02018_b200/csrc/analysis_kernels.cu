@@ -115,6 +115,7 @@ struct AnaStreamParams {
   int fmask;
   long long xdelta;
   T inv_lip, tau, mom;
+  const double *tdev;  // non-null: mom = (t - 1) / t+ from the device-resident t (graph-replayable)
 };
 
 template <typename T>
@@ -127,15 +128,15 @@ __device__ __forceinline__ T soft_thr(T v, T tau) {
 // fused FISTA update of one coefficient pair: g of grad f(y); (y, x) old values from the
 // prefetched tile; writes x+ and y+ at yp and yp + xdelta
 template <typename T, int L>
-__device__ __forceinline__ void fista_pair(const AnaStreamParams<T, L> &p, T *yp, typename Pair<T>::t g,
+__device__ __forceinline__ void fista_pair(const AnaStreamParams<T, L> &p, T mom, T *yp, typename Pair<T>::t g,
                                            const T *tile_y, const T *tile_x) {
   using P = typename Pair<T>::t;
   const P yv = *reinterpret_cast<const P *>(tile_y), xv = *reinterpret_cast<const P *>(tile_x);
   P xn, yn;
   xn.x = soft_thr<T>(yv.x - g.x * p.inv_lip, p.tau);
   xn.y = soft_thr<T>(yv.y - g.y * p.inv_lip, p.tau);
-  yn.x = xn.x + p.mom * (xn.x - xv.x);
-  yn.y = xn.y + p.mom * (xn.y - xv.y);
+  yn.x = xn.x + mom * (xn.x - xv.x);
+  yn.y = xn.y + mom * (xn.y - xv.y);
   *reinterpret_cast<P *>(yp + p.xdelta) = xn;
   *reinterpret_cast<P *>(yp) = yn;
 }
@@ -160,6 +161,11 @@ __global__ void __launch_bounds__(ACfg<T, L>::NT, sizeof(T) == 4 ? 768 / ACfg<T,
   __syncthreads();
   pdl_launch_dependents();
   pdl_wait();  // the previous kernel of the stream wrote our inputs
+  T mom = p.mom;
+  if (FU && p.tdev) {
+    const double t = *p.tdev, t_new = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
+    mom = T((t - 1.0) / t_new);
+  }
   unsigned phase = 0;
   // B item: segment fastest; C item: column pair fastest, then set (lo / hi), then group
   const bool actB = tid < C::ITEMS_B;
@@ -320,9 +326,9 @@ __global__ void __launch_bounds__(ACfg<T, L>::NT, sizeof(T) == 4 ? 768 / ACfg<T,
           if (FU && (fu0 || fu1)) {
 #pragma unroll
             for (int v = 0; v < VC; v++) {
-              if (fu0) fista_pair<T, L>(p, d0 + v * pX0, a0[v], ft0 + v * TQ, ft0 + C::FT + v * TQ);
+              if (fu0) fista_pair<T, L>(p, mom, d0 + v * pX0, a0[v], ft0 + v * TQ, ft0 + C::FT + v * TQ);
               else *reinterpret_cast<P *>(d0 + v * pX0) = a0[v];
-              if (fu1) fista_pair<T, L>(p, d1 + v * pX1, a1[v], ft1 + v * TQ, ft1 + C::FT + v * TQ);
+              if (fu1) fista_pair<T, L>(p, mom, d1 + v * pX1, a1[v], ft1 + v * TQ, ft1 + C::FT + v * TQ);
               else *reinterpret_cast<P *>(d1 + v * pX1) = a1[v];
             }
           } else
@@ -341,14 +347,14 @@ __global__ void __launch_bounds__(ACfg<T, L>::NT, sizeof(T) == 4 ? 768 / ACfg<T,
           if (!in1) z0.y = z1.y = T(0);
           T *e0 = oX0 + (long long)kr * pX0 + qc, *e1 = oX1 + (long long)kr * pX1 + qc;
           if (FU && fu0) {  // padding entries of x and y stay 0
-            fista_pair<T, L>(p, e0, z0, ft0 + v * TQ, ft0 + C::FT + v * TQ);
+            fista_pair<T, L>(p, mom, e0, z0, ft0 + v * TQ, ft0 + C::FT + v * TQ);
             if (!in0) e0[0] = e0[p.xdelta] = T(0);
             if (!in1) e0[1] = e0[p.xdelta + 1] = T(0);
           } else {
             *reinterpret_cast<P *>(e0) = z0;
           }
           if (FU && fu1) {
-            fista_pair<T, L>(p, e1, z1, ft1 + v * TQ, ft1 + C::FT + v * TQ);
+            fista_pair<T, L>(p, mom, e1, z1, ft1 + v * TQ, ft1 + C::FT + v * TQ);
             if (!in0) e1[0] = e1[p.xdelta] = T(0);
             if (!in1) e1[1] = e1[p.xdelta + 1] = T(0);
           } else {
@@ -409,6 +415,7 @@ cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
   p.inv_lip = T(a.fista_inv_lip);
   p.tau = T(a.fista_tau);
   p.mom = T(a.fista_mom);
+  p.tdev = a.fista_tdev;
   p.nstrips = (a.m1 + C::TQ - 1) / C::TQ;
   const size_t smem = C::smem_bytes(FU);
   auto kern = k_ana_stream<T, L, FU>;

@@ -153,6 +153,7 @@ int lh_index(const wl_plan *p, int j) { return 1 + 3 * (p->J - j); }
 struct FistaFuse {
   void *xo;
   double inv_lip, tau, mom;
+  const double *tdev;  // non-null: mom from the device-resident t
 };
 
 wl_status run_analysis(const wl_plan *p, int64_t batch, const void *img, void *x, char *ws, const WsLayout &L,
@@ -198,6 +199,7 @@ wl_status run_analysis(const wl_plan *p, int64_t batch, const void *img, void *x
       a.fista_inv_lip = fz->inv_lip;
       a.fista_tau = fz->tau;
       a.fista_mom = fz->mom;
+      a.fista_tdev = fz->tdev;
     }
     cudaError_t e = launch_analysis(p->dtype, a, s);
     if (e != cudaSuccess) return cuda_fail(e, "analysis level launch");
@@ -639,26 +641,29 @@ wl_status wl_fista_update(const wl_plan *p, int64_t batch, const void *g, void *
   return ok();
 }
 
-wl_status wl_fista_step(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, const void *b, void *x, void *y,
-                        double t, double lambda, double lip, double *f_dev, wl_adj adj, void *ws, void *stream) {
+static wl_status fista_step_core(const char *fn, const wl_plan *p, const wl_blur_plan *bl, int64_t batch,
+                                 const void *b, void *x, void *y, double t, double *t_dev, double lambda, double lip,
+                                 double *f_dev, wl_adj adj, void *ws, void *stream) {
   if (check_plan(p)) return WL_EINVAL;
-  if (adj != WL_ADJ_TRUE && adj != WL_ADJ_PINV) return fail(WL_EINVAL, "wl_fista_step: adj=%d is not a wl_adj", (int)adj);
-  if (!bl) return fail(WL_EINVAL, "wl_fista_step: blur plan is NULL");
+  if (adj != WL_ADJ_TRUE && adj != WL_ADJ_PINV) return fail(WL_EINVAL, "%s: adj=%d is not a wl_adj", fn, (int)adj);
+  if (!bl) return fail(WL_EINVAL, "%s: blur plan is NULL", fn);
   if (bl->h != p->h || bl->w != p->w || bl->dtype != p->dtype)
-    return fail(WL_EINVAL, "wl_fista_step: blur plan does not match the wavelet plan");
-  if (batch < 0) return fail(WL_EINVAL, "wl_fista_step: batch=%lld < 0", (long long)batch);
-  if (!(lip > 0) || !(lambda >= 0) || !(t >= 1)) return fail(WL_EINVAL, "wl_fista_step: need lip > 0, lambda >= 0, t >= 1");
+    return fail(WL_EINVAL, "%s: blur plan does not match the wavelet plan", fn);
+  if (batch < 0) return fail(WL_EINVAL, "%s: batch=%lld < 0", fn, (long long)batch);
+  if (!(lip > 0) || !(lambda >= 0) || !(t_dev || t >= 1))
+    return fail(WL_EINVAL, "%s: need lip > 0, lambda >= 0, t >= 1", fn);
   if (batch == 0) return ok();
   const size_t ib = (size_t)batch * p->h * p->w * p->es, xb = (size_t)batch * p->p_alloc * p->es;
   wl_status st;
   if ((st = check_dev(b, "b")) || (st = check_dev(x, "x")) || (st = check_dev(y, "y"))) return st;
+  if (t_dev && (st = check_dev(t_dev, "t_dev", 8))) return st;
   if (overlap(x, xb, y, xb) || overlap(b, ib, x, xb) || overlap(b, ib, y, xb))
-    return fail(WL_EINVAL, "wl_fista_step: b, x and y must not overlap");
+    return fail(WL_EINVAL, "%s: b, x and y must not overlap", fn);
   if (f_dev && (st = check_dev(f_dev, "f_dev", 8))) return st;
   if ((st = check_ws(p, bl, WL_OP_FISTA, batch, ws))) return st;
   WsLayout L = ws_layout(p, bl, WL_OP_FISTA, batch);
   if (overlap(ws, L.total, x, xb) || overlap(ws, L.total, y, xb) || overlap(ws, L.total, b, ib))
-    return fail(WL_EINVAL, "wl_fista_step: ws overlaps an argument");
+    return fail(WL_EINVAL, "%s: ws overlaps an argument", fn);
   cudaStream_t s = (cudaStream_t)stream;
   char *w = (char *)ws;
   // g = grad f(y) = W* R* (R W y - b), with the prox + momentum update fused into W*'s stores
@@ -666,9 +671,26 @@ wl_status wl_fista_step(const wl_plan *p, const wl_blur_plan *bl, int64_t batch,
   if ((st = run_synthesis(p, batch, y, w + L.u, w, L, s))) return st;
   if ((st = residual_core(bl, batch, w + L.u, b, w + L.s, f_dev, s))) return st;
   const double t_new = (1.0 + std::sqrt(1.0 + 4.0 * t * t)) / 2.0;
-  const FistaFuse fz{x, 1.0 / lip, lambda / lip, (t - 1.0) / t_new};
+  const FistaFuse fz{x, 1.0 / lip, lambda / lip, t_dev ? 0.0 : (t - 1.0) / t_new, t_dev};
   if ((st = run_analysis(p, batch, w + L.s, y, w, L, adj == WL_ADJ_TRUE, s, &fz))) return st;
+  if (t_dev) {
+    cudaError_t e = launch_fista_advance_t(t_dev, s);
+    if (e != cudaSuccess) return cuda_fail(e, "fista t update");
+  }
   return ok();
+}
+
+wl_status wl_fista_step(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, const void *b, void *x, void *y,
+                        double t, double lambda, double lip, double *f_dev, wl_adj adj, void *ws, void *stream) {
+  return fista_step_core("wl_fista_step", p, bl, batch, b, x, y, t, nullptr, lambda, lip, f_dev, adj, ws, stream);
+}
+
+wl_status wl_fista_step_dev(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, const void *b, void *x, void *y,
+                            double *t_dev, double lambda, double lip, double *f_dev, wl_adj adj, void *ws,
+                            void *stream) {
+  if (!t_dev) return fail(WL_EINVAL, "wl_fista_step_dev: t_dev is NULL");
+  return fista_step_core("wl_fista_step_dev", p, bl, batch, b, x, y, 1.0, t_dev, lambda, lip, f_dev, adj, ws,
+                         stream);
 }
 
 wl_status wl_lipschitz(const wl_plan *p, const wl_blur_plan *bl, int iters, uint64_t seed, double *lip_host, void *ws,

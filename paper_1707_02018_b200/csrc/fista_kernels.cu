@@ -5,6 +5,7 @@
 //   k_dot            per-image <a, b> in fp64 (block partials, one atomic per block and image)
 //   k_scale          v *= alpha
 //   k_fill_seeded    counter-hash uniform(-1, 1) start vector for the power iteration
+//   k_fista_advance_t  t <- t+ for FISTA with a device-resident t (graph-replayable iterations)
 // All elementwise kernels are grid-stride, 16-byte vectorised, sized to 4 waves of the SMs.
 #include <cuda_runtime.h>
 
@@ -85,6 +86,8 @@ __global__ void k_fill_seeded(T *__restrict__ v, long long n, unsigned long long
   }
 }
 
+__global__ void k_fista_advance_t(double *t) { *t = (1.0 + sqrt(1.0 + 4.0 * *t * *t)) / 2.0; }
+
 int grid_for(long long work, int nt) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -109,6 +112,12 @@ cudaError_t launch_fista_update(int dtype, const void *g, void *x, void *y, long
                                                              static_cast<float *>(y), n, (float)(1.0 / lip),
                                                              (float)(lambda / lip), (float)mom);
   }
+  g_launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fista_advance_t(double *t_dev, cudaStream_t s) {
+  k_fista_advance_t<<<1, 1, 0, s>>>(t_dev);
   g_launches++;
   return cudaGetLastError();
 }

@@ -40,6 +40,7 @@ struct AnalysisArgs {
   int fista_mask = 0;
   int64_t fista_xdelta = 0;
   double fista_inv_lip = 0, fista_tau = 0, fista_mom = 0;
+  const double *fista_tdev = nullptr;  // non-null: the momentum comes from the device-resident t
 };
 
 struct SynthesisArgs {
@@ -113,6 +114,8 @@ size_t bce_smem_bytes(int dtype, const BceArgs &a);
 cudaError_t launch_xcorr(int dtype, const XcorrArgs &x, cudaStream_t s);
 cudaError_t launch_bce_grad(int dtype, const BceArgs &a, cudaStream_t s);
 
+// t <- (1 + sqrt(1 + 4 t^2)) / 2 on the device (one thread; FISTA with device-resident t)
+cudaError_t launch_fista_advance_t(double *t_dev, cudaStream_t s);
 cudaError_t launch_fista_update(int dtype, const void *g, void *x, void *y, long long n, double t, double lambda,
                                 double lip, cudaStream_t s);
 cudaError_t launch_dot(int dtype, const void *a, const void *b, long long n, int batch, double *out, cudaStream_t s);

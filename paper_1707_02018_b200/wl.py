@@ -47,7 +47,7 @@ class _PlanInfo(ctypes.Structure):
 EXPORTS = ("wl_plan_create", "wl_plan_destroy", "wl_plan_query", "wl_plan_filters", "wl_workspace_bytes",
            "wl_synthesize", "wl_adjoint", "wl_analyze", "wl_analyze_adjoint", "wl_blur_create", "wl_blur_create_gaussian",
            "wl_blur_destroy", "wl_blur_taps", "wl_blur", "wl_blur_adjoint", "wl_blur_residual_adjoint",
-           "wl_grad", "wl_grad_adj", "wl_fista_update", "wl_fista_step", "wl_lipschitz", "wl_conv_full", "wl_conv_adjoint_h",
+           "wl_grad", "wl_grad_adj", "wl_fista_update", "wl_fista_step", "wl_fista_step_dev", "wl_lipschitz", "wl_conv_full", "wl_conv_adjoint_h",
            "wl_conv_adjoint_s", "wl_bce_grad", "wl_last_error", "wl_launch_count",
            "wl_version")
 
@@ -89,6 +89,7 @@ def lib():
     L.wl_fista_update.argtypes = [vp, i64, vp, vp, vp, cd, cd, cd, vp]
     L.wl_grad_adj.argtypes = [vp, vp, i64, vp, vp, vp, vp, ci, vp, vp]
     L.wl_fista_step.argtypes = [vp, vp, i64, vp, vp, vp, cd, cd, cd, vp, ci, vp, vp]
+    L.wl_fista_step_dev.argtypes = [vp, vp, i64, vp, vp, vp, vp, cd, cd, vp, ci, vp, vp]
     L.wl_lipschitz.argtypes = [vp, vp, ci, ctypes.c_uint64, dp, vp, vp]
     for fn in ("wl_conv_full", "wl_conv_adjoint_h", "wl_conv_adjoint_s"):
         getattr(L, fn).argtypes = [ci, i64, i64, i64, vp, vp, vp, vp]
@@ -429,9 +430,13 @@ def fista_update(plan: Plan, g, x, y, t: float, lam: float, lip: float, stream=N
     return next_t(t)
 
 
-def fista_step(plan: Plan, blur: Blur, b, x, y, t: float, lam: float, lip: float, f=None, ws=None, stream=None,
+def fista_step(plan: Plan, blur: Blur, b, x, y, t, lam: float, lip: float, f=None, ws=None, stream=None,
                adjoint="true"):
-    """One FISTA iteration on the GPU (grad f(y) then the fused prox + momentum update); returns t+."""
+    """One FISTA iteration on the GPU (grad f(y) then the fused prox + momentum update).
+
+    t is either the host scalar t_k (returns t_{k+1}) or a float64 CUDA tensor of one element
+    holding t_k, advanced in place on the device (wl_fista_step_dev; returns the tensor): the
+    launch sequence is then identical from one iteration to the next and graph-replayable."""
     _require(b, "b", plan.torch_dtype, (plan.h, plan.w))
     _require(x, "x", plan.torch_dtype, (plan.p_alloc,))
     _require(y, "y", plan.torch_dtype, (plan.p_alloc,))
@@ -439,15 +444,21 @@ def fista_step(plan: Plan, blur: Blur, b, x, y, t: float, lam: float, lip: float
     if f is not None:
         _require(f, "f", _torch().float64)
     ws = plan._ws(OP_FISTA, B, blur=blur, ws=ws)
+    if isinstance(t, _torch().Tensor):
+        _require(t, "t", _torch().float64)
+        _check(lib().wl_fista_step_dev(plan._h, blur._h, B, _ptr(b), _ptr(x), _ptr(y), _ptr(t), float(lam),
+                                       float(lip), _ptr(f), ADJOINTS[adjoint], _ptr(ws), _stream_ptr(stream)))
+        return t
     _check(lib().wl_fista_step(plan._h, blur._h, B, _ptr(b), _ptr(x), _ptr(y), float(t), float(lam), float(lip),
                                _ptr(f), ADJOINTS[adjoint], _ptr(ws), _stream_ptr(stream)))
     return next_t(t)
 
 
 def fista(plan: Plan, blur: Blur, b, lam: float, iters: int, lip: float = None, x0=None, stream=None,
-          adjoint="true"):
+          adjoint="true", graph: bool = False):
     """FISTA for min_x 1/2 ||R W x - b||^2 + lam ||x||_1 (Eq. (1); P:117 runs 2500 iterations).
-    Returns (x, y, t)."""
+    graph=True keeps t on the device and replays one captured iteration (wl.Graph) iters-1 times
+    after a first eager iteration.  Returns (x, y, t)."""
     torch = _torch()
     B = int(np.prod(b.shape[:-2])) if b.dim() > 2 else 1
     if lip is None:
@@ -455,10 +466,22 @@ def fista(plan: Plan, blur: Blur, b, lam: float, iters: int, lip: float = None, 
     x = torch.zeros(b.shape[:-2] + (plan.p_alloc,), dtype=b.dtype, device=b.device) if x0 is None else x0.clone()
     y = x.clone()
     ws = plan._ws(OP_FISTA, B, blur=blur)
-    t = 1.0
-    for _ in range(int(iters)):
-        t = fista_step(plan, blur, b, x, y, t, lam, lip, ws=ws, stream=stream, adjoint=adjoint)
-    return x, y, t
+    iters = int(iters)
+    if not graph:
+        t = 1.0
+        for _ in range(iters):
+            t = fista_step(plan, blur, b, x, y, t, lam, lip, ws=ws, stream=stream, adjoint=adjoint)
+        return x, y, t
+    t_dev = torch.ones(1, dtype=torch.float64, device=b.device)
+    if iters == 0:
+        return x, y, 1.0
+    step = lambda: fista_step(plan, blur, b, x, y, t_dev, lam, lip, ws=ws, adjoint=adjoint)  # noqa: E731
+    step()                                   # iteration 1, eager (warms every per-kernel cache)
+    if iters > 1:
+        g = Graph(step, warmup=0)
+        for _ in range(iters - 1):
+            g.replay()
+    return x, y, float(t_dev.item())
 
 
 # ------------------------------------------------------------------ Example 2

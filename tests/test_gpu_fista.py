@@ -148,3 +148,18 @@ def test_fista_pinv_iterations_match_oracle(torch, dtype, tol):
     xg, yg, tg = wl.fista(plan, blur, dev(torch, b, dtype), 2e-3, K, lip=1.05, adjoint="pinv")
     assert rel(plan.to_packed(xg.double().cpu().numpy()), x) <= tol
     assert rel(plan.to_packed(yg.double().cpu().numpy()), y) <= tol
+
+
+@pytest.mark.parametrize("dtype,tol", [("float64", 1e-12), ("float32", 1e-5)])
+def test_fista_graph_replay_matches_eager(torch, dtype, tol):
+    """Device-resident t + one captured iteration replayed (wl.fista(graph=True)) = the eager loop."""
+    h, w, J, K = 48, 40, 3, 12
+    plan = wl.Plan(h, w, J, "cdf97", "symmetric", dtype)
+    blur = wl.Blur(h, w, 15, 3.0, dtype=dtype)
+    rng = np.random.default_rng(21)
+    b = dev(torch, inputs.cast(O.blur(inputs.blobs(rng, 2, h, w, 6)), dtype), dtype)
+    xe, ye, te = wl.fista(plan, blur, b, 2e-3, K, lip=1.05)
+    xg, yg, tg = wl.fista(plan, blur, b, 2e-3, K, lip=1.05, graph=True)
+    assert tg == pytest.approx(te, rel=1e-14)
+    assert float((xg - xe).abs().max()) <= tol * max(float(xe.abs().max()), 1e-30)
+    assert float((yg - ye).abs().max()) <= tol * max(float(ye.abs().max()), 1e-30)
