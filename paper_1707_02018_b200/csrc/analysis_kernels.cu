@@ -53,7 +53,7 @@ __device__ __forceinline__ int ext_src(int t, int n, int ext, int Lp, T &w) {
   return s;
 }
 
-template <typename T, int L>
+template <typename T, int L, int NS_ = 0>
 struct ACfg {
   using P = typename Pair<T>::t;
   static constexpr int VEC = Vec16<T>::n;
@@ -81,7 +81,9 @@ struct ACfg {
 #ifndef WL_ANA_NS
 #define WL_ANA_NS 2  // A/B on B200: 3 or 4 stages did not beat 2
 #endif
-  static constexpr int NS = WL_ANA_NS;                   // input stages (prefetch depth NS-1)
+  // input stages (prefetch depth NS-1); short runs (coarse levels) use 4 so every block of the
+  // run is in flight at once instead of one TMA round trip per block
+  static constexpr int NS = NS_ > 0 ? NS_ : WL_ANA_NS;
   static constexpr size_t OFF_U = 0;  // [NS][GI][UP]
   static constexpr size_t OFF_H = OFF_U + round_up_c(NS * GI * UP * (int)sizeof(T), 128);  // [2 sets][HR][HP]
   static constexpr size_t OFF_BAR = OFF_H + 2 * (size_t)HR * HP * sizeof(T);
@@ -141,10 +143,10 @@ __device__ __forceinline__ void fista_pair(const AnaStreamParams<T, L> &p, T mom
   *reinterpret_cast<P *>(yp) = yn;
 }
 
-template <typename T, int L, bool FU>
+template <typename T, int L, bool FU, int NS>
 __global__ void __launch_bounds__(ACfg<T, L>::NT, sizeof(T) == 4 ? 768 / ACfg<T, L>::NT : 1)
     k_ana_stream(const __grid_constant__ AnaStreamParams<T, L> p) {
-  using C = ACfg<T, L>;
+  using C = ACfg<T, L, NS>;
   using P = typename C::P;
   using Vt = typename Vec16<T>::type;
   constexpr int G = C::G, GI = C::GI, VEC = C::VEC, V = C::V, VC = C::VC, TQ = C::TQ;
@@ -417,14 +419,25 @@ cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
   p.mom = T(a.fista_mom);
   p.tdev = a.fista_tdev;
   p.nstrips = (a.m1 + C::TQ - 1) / C::TQ;
-  const size_t smem = C::smem_bytes(FU);
-  auto kern = k_ana_stream<T, L, FU>;
+  // runs of at most 3 blocks (coarse levels) prefetch all their blocks at once (NS = 4)
   long long resident = 0;
-  cudaError_t e = kernel_resident(reinterpret_cast<const void *>(kern), C::NT, smem, &resident);
+  cudaError_t e = kernel_resident(reinterpret_cast<const void *>(k_ana_stream<T, L, FU, 0>), C::NT,
+                                  C::smem_bytes(FU), &resident);
   if (e != cudaSuccess) return e;
   p.runs = RunMap::make((long long)a.batch * p.nstrips, a.m0, resident, C::G, 1);
-  const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
-  e = launch_pdl(kern, grid, C::NT, smem, s, p);
+  const int band = (a.m0 + p.runs.nb_lo - 1) / p.runs.nb_lo;
+  if ((band + C::G - 1) / C::G <= short_run_max(3)) {
+    using C4 = ACfg<T, L, 4>;
+    e = kernel_resident(reinterpret_cast<const void *>(k_ana_stream<T, L, FU, 4>), C4::NT, C4::smem_bytes(FU),
+                        &resident);
+    if (e != cudaSuccess) return e;
+    p.runs = RunMap::make((long long)a.batch * p.nstrips, a.m0, resident, C::G, 1);
+    const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
+    e = launch_pdl(k_ana_stream<T, L, FU, 4>, grid, C4::NT, C4::smem_bytes(FU), s, p);
+  } else {
+    const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
+    e = launch_pdl(k_ana_stream<T, L, FU, 0>, grid, C::NT, C::smem_bytes(FU), s, p);
+  }
   g_launches++;
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

@@ -36,7 +36,7 @@ namespace {
 
 constexpr int H_MAX = kMaxL / 2;
 
-template <typename T, int L>
+template <typename T, int L, int NS_ = 0>
 struct SCfg {
   using P = typename Pair<T>::t;
   static constexpr int VEC = Vec16<T>::n;
@@ -64,7 +64,8 @@ struct SCfg {
 #ifndef WL_SYN_NS
 #define WL_SYN_NS 2  // A/B on B200: 3 or 4 stages did not beat 2
 #endif
-  static constexpr int NS = WL_SYN_NS;                   // coefficient stages (prefetch depth NS-1)
+  // coefficient stages (prefetch depth NS-1); short runs (coarse levels) use 4
+  static constexpr int NS = NS_ > 0 ? NS_ : WL_SYN_NS;
   static constexpr size_t OFF_C = 0;                     // [NS][4][G][KCP]
   static constexpr size_t OFF_V = OFF_C + round_up_c(NS * 4 * G * KCP * (int)sizeof(T), 128);
   static constexpr size_t OFF_BAR = OFF_V + 2 * (size_t)HR * TWP * sizeof(T);  // VL, VH histories
@@ -89,10 +90,10 @@ struct SynStreamParams {
   P e_hi[H_MAX], o_hi[H_MAX];
 };
 
-template <typename T, int L>
+template <typename T, int L, int NS>
 __global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 768 / SCfg<T, L>::NT : 1)
     k_synth_stream(const __grid_constant__ SynStreamParams<T, L> p) {
-  using C = SCfg<T, L>;
+  using C = SCfg<T, L, NS>;
   using P = typename C::P;
   using Vt = typename Vec16<T>::type;
   constexpr int G = C::G, H = C::H, VEC = C::VEC, VC = C::VC, SP = C::SP;
@@ -352,15 +353,26 @@ cudaError_t launch_synth_stream_t(const SynthesisArgs &a, cudaStream_t s) {
   }
   const int span0 = a.o0 + a.N0 - p.t00, span1 = a.o1 + a.N1 - p.t01;
   p.nstrips = (span1 + C::TW - 1) / C::TW;
-  const size_t smem = C::smem_bytes();
-  auto kern = k_synth_stream<T, L>;
   long long resident = 0;
-  cudaError_t e = kernel_resident(reinterpret_cast<const void *>(kern), C::NT, smem, &resident);
+  cudaError_t e = kernel_resident(reinterpret_cast<const void *>(k_synth_stream<T, L, 0>), C::NT, C::smem_bytes(),
+                                  &resident);
   if (e != cudaSuccess) return e;
   // one run per resident CTA when the columns allow it; even bands of >= 4 iterations
   p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident, 2 * C::G, 2);
-  const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
-  e = launch_pdl(kern, grid, C::NT, smem, s, p);
+  const int band = (span0 + p.runs.nb_lo - 1) / p.runs.nb_lo;
+  if ((band / 2 + C::H - 1) / C::G + 1 <= short_run_max(2)) {
+    // short runs (coarse levels): every batch of the run in flight at once
+    using C4 = SCfg<T, L, 4>;
+    e = kernel_resident(reinterpret_cast<const void *>(k_synth_stream<T, L, 4>), C4::NT, C4::smem_bytes(),
+                        &resident);
+    if (e != cudaSuccess) return e;
+    p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident, 2 * C::G, 2);
+    const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
+    e = launch_pdl(k_synth_stream<T, L, 4>, grid, C4::NT, C4::smem_bytes(), s, p);
+  } else {
+    const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
+    e = launch_pdl(k_synth_stream<T, L, 0>, grid, C::NT, C::smem_bytes(), s, p);
+  }
   g_launches++;
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -62,6 +63,14 @@ bool encode_tmap_3d(void *map, int elem_bytes, const void *base, uint64_t d0, ui
   if (cache.size() > 4096) cache.clear();
   cache[key] = *reinterpret_cast<CUtensorMap *>(map);
   return true;
+}
+
+int short_run_max(int dflt) {
+  static const int v = [] {
+    const char *e = getenv("WL_SHORT_MAX");
+    return e ? atoi(e) : -1;
+  }();
+  return v >= 0 ? v : dflt;
 }
 
 cudaError_t kernel_resident(const void *kern, int nt, size_t smem, long long *resident) {

@@ -134,6 +134,11 @@ bool encode_tmap_3d(void *map, int elem_bytes, const void *base, uint64_t d0, ui
 // device), so a launch pays the attribute / occupancy queries once.
 cudaError_t kernel_resident(const void *kern, int nt, size_t smem, long long *resident);
 
+// Longest run (in blocks / batches) that the streaming kernels treat as short and launch with
+// every block in flight at once (4 stages): `dflt` is the kernel's measured best (analysis 3,
+// synthesis 2 on B200); WL_SHORT_MAX overrides both (0 disables; A/B switch).
+int short_run_max(int dflt);
+
 // Launch with programmatic stream serialization (PDL): the kernel may start while the
 // previous kernel of the stream drains; it must call pdl_wait() before its first global
 // memory access (every streaming kernel of libwl does, right after its shared-memory setup).
