@@ -28,14 +28,13 @@ def main():
                 print(f"  {k:70s} {units[hdr.index(k)]:>8s} {v[hdr.index(k)]}")
         st = []
         for i, k in enumerate(hdr):
-            if k.startswith("smsp__average_warp_latency_issue_stalled_") or (
-                    k.startswith("smsp__warp_issue_stalled_") and k.endswith("_per_warp_active.pct")):
+            if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("_not_issued"):
                 try:
-                    st.append((float(v[i]), k))
+                    st.append((float(v[i]), k[len("smsp__pcsamp_warps_issue_stalled_"):]))
                 except ValueError:
                     pass
-        for val, k in sorted(st, reverse=True)[:12]:
-            print(f"  {k:70s} {val:.2f}")
+        tot = sum(x for x, _ in st) or 1.0
+        print("  stalls (pc samples): " + "  ".join(f"{k} {100 * x / tot:.0f}%" for x, k in sorted(st, reverse=True)[:9]))
 
 
 if __name__ == "__main__":

@@ -2,7 +2,7 @@
 """Per-operator timing on one GPU (development tool; bench.py is the contract).
 
   python tools/opbench.py --cfg 4 --op adjoint --reps 50
-ops: adjoint, analyze, analyze_adjoint, synthesize, blur, residual, grad.  Prints one JSON line per op with
+ops: adjoint, analyze, analyze_adjoint, synthesize, blur, residual, grad, fista.  Prints one JSON line per op with
 device ms per call (CUDA events, warm L2 for small configs).
 """
 import argparse
@@ -65,6 +65,12 @@ def main():
             ws = plan._ws(wl.OP_GRAD, B, blur=blur)
             fn = lambda: wl.grad(plan, blur, x, img2, out=out_x, ws=ws)  # noqa: E731
             nbytes = (6 * c.h * c.w + 2 * (c.h * c.w + plan.p_valid)) * B * plan.torch_dtype.itemsize
+        elif op == "fista":
+            ws = plan._ws(wl.OP_FISTA, B, blur=blur)
+            xf, yf = torch.zeros_like(x), x.clone()
+            t_dev = torch.full((1,), 2.0, dtype=torch.float64, device="cuda")
+            fn = lambda: wl.fista_step(plan, blur, img2, xf, yf, t_dev, 1e-3, 1.0, ws=ws)  # noqa: E731
+            nbytes = (6 * c.h * c.w + 2 * (c.h * c.w + plan.p_valid) + 3 * plan.p_valid) * B * plan.torch_dtype.itemsize
         else:
             raise SystemExit(f"unknown op {op}")
         for _ in range(3):
