@@ -53,18 +53,31 @@ __device__ __forceinline__ int ext_src(int t, int n, int ext, int Lp, T &w) {
   return s;
 }
 
-template <typename T, int L, int NS_ = 0>
+template <typename T, int L, int NS_ = 0, bool FU_ = false>
 struct ACfg {
   using P = typename Pair<T>::t;
   static constexpr int VEC = Vec16<T>::n;
-  static constexpr int TQ = sizeof(T) == 4 ? 64 : 32;   // coefficient columns per strip
-#ifndef WL_ANA_G
-#define WL_ANA_G 8  // A/B on B200: 8 beat 16 at cfg5 (-10 us), equal at cfg4
+  // fp32 tile (A/B on B200): 16 coefficient outputs per B item, 8 rows per C item, 16 rows per
+  // iteration beat (8, 4, 8) by 6 % at cfg5 and 5 % at cfg4 (less shared-memory traffic per FFMA2:
+  // fewer window re-reads).  The fused FISTA variant keeps (8, 4, 8): its (y, x) tiles scale with G.
+#ifndef WL_ANA_TQ
+#define WL_ANA_TQ 64
 #endif
-  static constexpr int G = WL_ANA_G;                     // coefficient rows per iteration
+#ifndef WL_ANA_V
+#define WL_ANA_V 16
+#endif
+#ifndef WL_ANA_VC
+#define WL_ANA_VC 8
+#endif
+#ifndef WL_ANA_G
+#define WL_ANA_G 16
+#endif
+  static constexpr bool F32 = sizeof(T) == 4;
+  static constexpr int TQ = F32 ? WL_ANA_TQ : 32;                     // coefficient columns per strip
+  static constexpr int G = (F32 && !FU_) ? WL_ANA_G : 8;              // coefficient rows per iteration
   static constexpr int GI = 2 * G;                       // input rows per iteration
-  static constexpr int V = 8;                            // coefficient outputs per B item
-  static constexpr int VC = 4;                           // coefficient rows per C item
+  static constexpr int V = (F32 && !FU_) ? WL_ANA_V : 8;      // coefficient outputs per B item
+  static constexpr int VC = (F32 && !FU_) ? WL_ANA_VC : 4;    // coefficient rows per C item
   static constexpr int SHIFT = ((2 - L) % VEC + VEC) % VEC;  // box column of input column 2q0+2-L
   static constexpr int UW = round_up_c(SHIFT + 2 * TQ + L - 2, VEC);  // input box width
   static constexpr int UP = UW;                          // dense TMA box rows
@@ -144,9 +157,9 @@ __device__ __forceinline__ void fista_pair(const AnaStreamParams<T, L> &p, T mom
 }
 
 template <typename T, int L, bool FU, int NS>
-__global__ void __launch_bounds__(ACfg<T, L>::NT, sizeof(T) == 4 ? 768 / ACfg<T, L>::NT : 1)
+__global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? 768 / ACfg<T, L, NS, FU>::NT : 1)
     k_ana_stream(const __grid_constant__ AnaStreamParams<T, L> p) {
-  using C = ACfg<T, L, NS>;
+  using C = ACfg<T, L, NS, FU>;
   using P = typename C::P;
   using Vt = typename Vec16<T>::type;
   constexpr int G = C::G, GI = C::GI, VEC = C::VEC, V = C::V, VC = C::VC, TQ = C::TQ;
@@ -381,7 +394,7 @@ __global__ void __launch_bounds__(ACfg<T, L>::NT, sizeof(T) == 4 ? 768 / ACfg<T,
 
 template <typename T, int L, bool FU>
 cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
-  using C = ACfg<T, L>;
+  using C = ACfg<T, L, 0, FU>;
   AnaStreamParams<T, L> p;
   memset(&p, 0, sizeof p);
   p.in = static_cast<const T *>(a.in);
@@ -427,7 +440,7 @@ cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
   p.runs = RunMap::make((long long)a.batch * p.nstrips, a.m0, resident, C::G, 1);
   const int band = (a.m0 + p.runs.nb_lo - 1) / p.runs.nb_lo;
   if ((band + C::G - 1) / C::G <= short_run_max(3)) {
-    using C4 = ACfg<T, L, 4>;
+    using C4 = ACfg<T, L, 4, FU>;
     e = kernel_resident(reinterpret_cast<const void *>(k_ana_stream<T, L, FU, 4>), C4::NT, C4::smem_bytes(FU),
                         &resident);
     if (e != cudaSuccess) return e;

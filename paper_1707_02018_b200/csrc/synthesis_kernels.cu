@@ -46,8 +46,14 @@ struct SCfg {
 #define WL_SYN_G 16
 #endif
   static constexpr int G = WL_SYN_G;                     // coefficient rows per iteration
-  static constexpr int SP = 8;                           // output column pairs per S1 item
-  static constexpr int VC = 4;                           // s-values (output row pairs) per S0 item
+#ifndef WL_SYN_SP
+#define WL_SYN_SP 8
+#endif
+#ifndef WL_SYN_VC
+#define WL_SYN_VC 4
+#endif
+  static constexpr int SP = sizeof(T) == 4 ? WL_SYN_SP : 8;   // output column pairs per S1 item
+  static constexpr int VC = sizeof(T) == 4 ? WL_SYN_VC : 4;   // s-values (output row pairs) per S0 item
   static constexpr int KCW = round_up_c(TW / 2 + H - 1, VEC);  // coefficient columns loaded
   static constexpr int KCP = KCW;                        // dense TMA box rows
   static constexpr int NWC = round_up_c(SP + H - 1, VEC);  // S1 window per subband
