@@ -101,7 +101,8 @@ typedef enum {
   WL_OP_GRAD = 3,
   WL_OP_ANALYZE_ADJOINT = 4,
   WL_OP_FISTA = 5,
-  WL_OP_LIPSCHITZ = 6
+  WL_OP_LIPSCHITZ = 6,
+  WL_OP_GRAD_HOST = 7
 } wl_op;
 
 typedef struct wl_plan wl_plan;           /* opaque, immutable after create */
@@ -198,6 +199,17 @@ WL_API wl_status wl_blur_residual_adjoint(const wl_blur_plan *blur, int64_t batc
  * The plans must agree in h, w and dtype.  ws: wl_workspace_bytes(plan, blur, WL_OP_GRAD, batch). */
 WL_API wl_status wl_grad(const wl_plan *plan, const wl_blur_plan *blur, int64_t batch, const void *x,
                   const void *b, void *g, double *f_dev, void *ws, void *stream);
+
+/* wl_grad with HOST buffers: x_host [batch, p_alloc], b_host [batch, h, w] -> g_host [batch, p_alloc],
+ * f_host (nullable, double[batch]).  The images are pipelined through two device slots inside `ws`
+ * (wl_workspace_bytes(plan, blur, WL_OP_GRAD_HOST, batch); independent of batch): image i+1 is copied
+ * in on an internal copy stream while image i is differentiated on `stream` and image i-1 copied out
+ * on a second copy stream, so the transfers overlap each other and the kernels.  Host buffers should
+ * be page-locked (cudaHostAlloc / cudaHostRegister) for the copies to be asynchronous; pageable
+ * buffers still give correct results.  Stream-ordered: the outputs are complete when `stream` reaches
+ * the point after the call; the host buffers must stay untouched until then. */
+WL_API wl_status wl_grad_host(const wl_plan *plan, const wl_blur_plan *blur, int64_t batch, const void *x_host,
+                       const void *b_host, void *g_host, double *f_host, void *ws, void *stream);
 
 /* Which operator closes the gradient (P:117, P:176-177 compare both under FISTA):
  *   WL_ADJ_TRUE  W*  (the true adjoint, Eq. (4)) -> grad f exactly;

@@ -88,9 +88,21 @@ bool overlap(const void *a, size_t na, const void *b, size_t nb) {
 // workspace carve-up ---------------------------------------------------------
 struct WsLayout {
   size_t a = 0, b = 0, e = 0, u = 0, s = 0, g = 0, v = 0, b0 = 0, d = 0, total = 0;  // byte offsets
+  size_t hx = 0, hb = 0, hg = 0, hf = 0;  // WL_OP_GRAD_HOST: two device slots each for x, b, g, f
 };
 
 WsLayout ws_layout(const wl_plan *p, const wl_blur_plan *bl, wl_op op, int64_t batch) {
+  if (op == WL_OP_GRAD_HOST) {  // the grad workspace of one image + two staging slots
+    WsLayout L = ws_layout(p, bl, WL_OP_GRAD, 1);
+    const size_t es = (size_t)p->es, xs = (size_t)p->p_alloc * es, is = (size_t)p->h * p->w * es;
+    size_t off = L.total;
+    L.hx = off; off = align256(off + 2 * xs);
+    L.hb = off; off = align256(off + 2 * is);
+    L.hg = off; off = align256(off + 2 * xs);
+    L.hf = off; off = align256(off + 2 * sizeof(double));
+    L.total = batch > 0 ? off : 0;
+    return L;
+  }
   WsLayout L;
   size_t es = (size_t)p->es, B = (size_t)batch;
   size_t off = 0;
@@ -620,6 +632,57 @@ wl_status wl_grad_adj(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, c
     return fail(WL_EINVAL, "wl_grad: ws overlaps an argument");
   st = grad_core(p, bl, batch, x, b, g, f_dev, (char *)ws, L, (cudaStream_t)stream, adj == WL_ADJ_TRUE);
   return st ? st : ok();
+}
+
+wl_status wl_grad_host(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, const void *x_host,
+                       const void *b_host, void *g_host, double *f_host, void *ws, void *stream) {
+  if (check_plan(p)) return WL_EINVAL;
+  if (!bl) return fail(WL_EINVAL, "wl_grad_host: blur plan is NULL");
+  if (bl->h != p->h || bl->w != p->w || bl->dtype != p->dtype)
+    return fail(WL_EINVAL, "wl_grad_host: blur plan does not match the wavelet plan");
+  if (batch < 0) return fail(WL_EINVAL, "wl_grad_host: batch=%lld < 0", (long long)batch);
+  if (batch == 0) return ok();
+  if (!x_host || !b_host || !g_host) return fail(WL_EINVAL, "wl_grad_host: x_host, b_host and g_host must be non-NULL");
+  wl_status st;
+  if ((st = check_ws(p, bl, WL_OP_GRAD_HOST, batch, ws))) return st;
+  const WsLayout L = ws_layout(p, bl, WL_OP_GRAD_HOST, batch);
+  const size_t es = (size_t)p->es, xs = (size_t)p->p_alloc * es, is = (size_t)p->h * p->w * es;
+  cudaStream_t s = (cudaStream_t)stream, cin = nullptr, cout = nullptr;
+  cudaEvent_t ev[7] = {};  // start, in[2], done[2], free[2]
+  cudaError_t e = cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking);
+  for (int i = 0; i < 7 && e == cudaSuccess; i++) e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+  char *w = (char *)ws;
+  if (e == cudaSuccess) e = cudaEventRecord(ev[0], s);  // the call is ordered after prior work on `stream`
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(cin, ev[0], 0);
+  for (int64_t i = 0; i < batch && e == cudaSuccess && !st; i++) {
+    const int k = (int)(i & 1);
+    char *dx = w + L.hx + k * xs, *db = w + L.hb + k * is, *dg = w + L.hg + k * xs;
+    double *df = reinterpret_cast<double *>(w + L.hf) + k;
+    if (i >= 2) e = cudaStreamWaitEvent(cin, ev[5 + k], 0);  // slot k copied out (image i-2)
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dx, (const char *)x_host + i * xs, xs, cudaMemcpyHostToDevice, cin);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(db, (const char *)b_host + i * is, is, cudaMemcpyHostToDevice, cin);
+    if (e == cudaSuccess) e = cudaEventRecord(ev[1 + k], cin);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev[1 + k], 0);
+    if (e != cudaSuccess) break;
+    st = grad_core(p, bl, 1, dx, db, dg, f_host ? df : nullptr, w, L, s);
+    if (st) break;
+    e = cudaEventRecord(ev[3 + k], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cout, ev[3 + k], 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync((char *)g_host + i * xs, dg, xs, cudaMemcpyDeviceToHost, cout);
+    if (e == cudaSuccess && f_host) e = cudaMemcpyAsync(f_host + i, df, sizeof(double), cudaMemcpyDeviceToHost, cout);
+    if (e == cudaSuccess) e = cudaEventRecord(ev[5 + k], cout);
+  }
+  // `stream` resumes after the last copy out
+  if (e == cudaSuccess && !st) e = cudaEventRecord(ev[0], cout);
+  if (e == cudaSuccess && !st) e = cudaStreamWaitEvent(s, ev[0], 0);
+  for (int i = 0; i < 7; i++)
+    if (ev[i]) cudaEventDestroy(ev[i]);  // released once their pending work completes
+  if (cin) cudaStreamDestroy(cin);
+  if (cout) cudaStreamDestroy(cout);
+  if (st) return st;
+  if (e != cudaSuccess) return cuda_fail(e, "wl_grad_host pipeline");
+  return ok();
 }
 
 wl_status wl_fista_update(const wl_plan *p, int64_t batch, const void *g, void *x, void *y, double t, double lambda,

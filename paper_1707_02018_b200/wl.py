@@ -23,7 +23,7 @@ _LIB_PATH = os.environ.get("WL_LIB") or os.path.join(_PKG, "libwl.so")   # WL_LI
 WL_OK, WL_EINVAL, WL_ESIZE, WL_EDTYPE, WL_EALIGN, WL_ENOMEM, WL_ECUDA = range(7)
 FILTERS = {"haar": 1, "db1": 1, "db2": 2, "db4": 4, "db8": 8, "cdf97": 97}
 BCS = {"zero": 0, "periodic": 1, "symmetric": 2, "symmetric_edag": 3}
-OP_SYNTHESIZE, OP_ADJOINT, OP_ANALYZE, OP_GRAD, OP_ANALYZE_ADJOINT, OP_FISTA, OP_LIPSCHITZ = range(7)
+OP_SYNTHESIZE, OP_ADJOINT, OP_ANALYZE, OP_GRAD, OP_ANALYZE_ADJOINT, OP_FISTA, OP_LIPSCHITZ, OP_GRAD_HOST = range(8)
 MAX_LEVELS = 32
 
 
@@ -47,7 +47,7 @@ class _PlanInfo(ctypes.Structure):
 EXPORTS = ("wl_plan_create", "wl_plan_destroy", "wl_plan_query", "wl_plan_filters", "wl_workspace_bytes",
            "wl_synthesize", "wl_adjoint", "wl_analyze", "wl_analyze_adjoint", "wl_blur_create", "wl_blur_create_gaussian",
            "wl_blur_destroy", "wl_blur_taps", "wl_blur", "wl_blur_adjoint", "wl_blur_residual_adjoint",
-           "wl_grad", "wl_grad_adj", "wl_fista_update", "wl_fista_step", "wl_fista_step_dev", "wl_lipschitz", "wl_conv_full", "wl_conv_adjoint_h",
+           "wl_grad", "wl_grad_host", "wl_grad_adj", "wl_fista_update", "wl_fista_step", "wl_fista_step_dev", "wl_lipschitz", "wl_conv_full", "wl_conv_adjoint_h",
            "wl_conv_adjoint_s", "wl_bce_grad", "wl_last_error", "wl_launch_count",
            "wl_version")
 
@@ -87,6 +87,7 @@ def lib():
     L.wl_blur_residual_adjoint.argtypes = [vp, i64, vp, vp, vp, vp, vp]
     L.wl_grad.argtypes = [vp, vp, i64, vp, vp, vp, vp, vp, vp]
     L.wl_fista_update.argtypes = [vp, i64, vp, vp, vp, cd, cd, cd, vp]
+    L.wl_grad_host.argtypes = [vp, vp, i64, vp, vp, vp, vp, vp, vp]
     L.wl_grad_adj.argtypes = [vp, vp, i64, vp, vp, vp, vp, ci, vp, vp]
     L.wl_fista_step.argtypes = [vp, vp, i64, vp, vp, vp, cd, cd, cd, vp, ci, vp, vp]
     L.wl_fista_step_dev.argtypes = [vp, vp, i64, vp, vp, vp, vp, cd, cd, vp, ci, vp, vp]
@@ -355,6 +356,35 @@ class Blur:
                 self._h = None
         except Exception:
             pass
+
+
+def grad_host(plan: Plan, blur: Blur, x, b, out=None, f=None, ws=None, stream=None):
+    """wl_grad on HOST tensors (pin them for asynchronous copies): x [B, p_alloc], b [B, h, w] (CPU)
+    -> g [B, p_alloc] (CPU), f (optional CPU float64 [B]).  The images are pipelined through two
+    device slots (copy-in of image i+1 and copy-out of image i-1 overlap the gradient of image i);
+    returns when the results are on the host."""
+    torch = _torch()
+    for name, t, shape in (("x", x, (plan.p_alloc,)), ("b", b, (plan.h, plan.w))):
+        if not isinstance(t, torch.Tensor) or t.is_cuda or not t.is_contiguous() or t.dtype != plan.torch_dtype:
+            raise ValueError(f"{name} must be a contiguous CPU tensor of {plan.torch_dtype}")
+        if tuple(t.shape[-len(shape):]) != shape:
+            raise ValueError(f"{name} has shape {tuple(t.shape)}, expected [..., {', '.join(map(str, shape))}]")
+    B = int(np.prod(x.shape[:-1])) if x.dim() > 1 else 1
+    if (int(np.prod(b.shape[:-2])) if b.dim() > 2 else 1) != B:
+        raise ValueError("x and b must have the same batch")
+    if out is None:
+        out = torch.empty(x.shape, dtype=x.dtype, pin_memory=x.is_pinned())
+    if out.is_cuda or not out.is_contiguous() or out.shape != x.shape or out.dtype != x.dtype:
+        raise ValueError("out must be a contiguous CPU tensor shaped like x")
+    if f is not None and (f.is_cuda or f.dtype != torch.float64 or f.numel() != B):
+        raise ValueError("f must be a CPU float64 tensor of batch elements")
+    ws = plan._ws(OP_GRAD_HOST, B, blur=blur, ws=ws)
+    st = _stream_ptr(stream)
+    _check(lib().wl_grad_host(plan._h, blur._h, B, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(b.data_ptr()),
+                              ctypes.c_void_p(out.data_ptr()),
+                              None if f is None else ctypes.c_void_p(f.data_ptr()), _ptr(ws), st))
+    (stream or torch.cuda.current_stream()).synchronize()
+    return out
 
 
 ADJOINTS = {"true": 0, "pinv": 1}  # wl_adj: close the gradient with W* or with W-dagger (P:117)

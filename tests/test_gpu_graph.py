@@ -37,3 +37,22 @@ def test_graph_replay_equals_eager(torch, filt, bc):
     graph.replay()
     torch.cuda.synchronize()
     assert torch.allclose(g, wl.grad(plan, blur, x, b), rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("B", [1, 2, 5])
+def test_grad_host_pipeline_equals_device(torch, B):
+    """wl_grad_host (host buffers, two pipelined device slots) = wl_grad on device copies."""
+    h, w, J = 96, 80, 3
+    plan = wl.Plan(h, w, J, "cdf97", "symmetric", "float32")
+    blur = wl.Blur(h, w, 15, 3.0, dtype="float32")
+    rng = np.random.default_rng(B)
+    xh = torch.from_numpy(plan.from_packed(rng.standard_normal((B, plan.p_valid)).astype(np.float32))).pin_memory()
+    bh = torch.from_numpy(rng.standard_normal((B, h, w)).astype(np.float32)).pin_memory()
+    fh = torch.zeros(B, dtype=torch.float64)
+    gh = wl.grad_host(plan, blur, xh, bh, f=fh)
+    f = torch.zeros(B, dtype=torch.float64, device="cuda")
+    g = wl.grad(plan, blur, xh.cuda(), bh.cuda(), f=f)
+    assert torch.equal(gh, g.cpu())
+    assert torch.allclose(fh, f.cpu(), rtol=1e-12, atol=0)
+    gp = wl.grad_host(plan, blur, xh.clone(), bh.clone())   # pageable buffers: same results
+    assert torch.equal(gp, gh)
