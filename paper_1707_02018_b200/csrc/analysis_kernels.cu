@@ -446,10 +446,10 @@ cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     p.runs = RunMap::make((long long)a.batch * p.nstrips, a.m0, resident, C::G, 1);
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
-    e = launch_pdl(k_ana_stream<T, L, FU, 4>, grid, C4::NT, C4::smem_bytes(FU), s, p);
+    e = launch_pdl(k_ana_stream<T, L, FU, 4>, grid, C4::NT, C4::smem_bytes(FU), s, p, 'a');
   } else {
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
-    e = launch_pdl(k_ana_stream<T, L, FU, 0>, grid, C::NT, C::smem_bytes(FU), s, p);
+    e = launch_pdl(k_ana_stream<T, L, FU, 0>, grid, C::NT, C::smem_bytes(FU), s, p, 'A');
   }
   g_launches++;
   if (e != cudaSuccess) return e;

@@ -514,7 +514,7 @@ cudaError_t launch_stream(const BlurArgs &a, cudaStream_t s) {
     e = cudaMemsetAsync(a.f, 0, sizeof(double) * (size_t)a.batch, s);
     if (e != cudaSuccess) return e;
   }
-  e = launch_pdl(kern, grid, C::NT, smem, s, p);
+  e = launch_pdl(kern, grid, C::NT, smem, s, p, 'b');
   g_launches++;
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

@@ -374,10 +374,10 @@ cudaError_t launch_synth_stream_t(const SynthesisArgs &a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident, 2 * C::G, 2);
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
-    e = launch_pdl(k_synth_stream<T, L, 4>, grid, C4::NT, C4::smem_bytes(), s, p);
+    e = launch_pdl(k_synth_stream<T, L, 4>, grid, C4::NT, C4::smem_bytes(), s, p, 's');
   } else {
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
-    e = launch_pdl(k_synth_stream<T, L, 0>, grid, C::NT, C::smem_bytes(), s, p);
+    e = launch_pdl(k_synth_stream<T, L, 0>, grid, C::NT, C::smem_bytes(), s, p, 'S');
   }
   g_launches++;
   if (e != cudaSuccess) return e;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -63,6 +64,17 @@ bool encode_tmap_3d(void *map, int elem_bytes, const void *base, uint64_t d0, ui
   if (cache.size() > 4096) cache.clear();
   cache[key] = *reinterpret_cast<CUtensorMap *>(map);
   return true;
+}
+
+bool pdl_enabled(char kind) {
+  static const char *off = [] {
+    // measured on B200 (cfg5 grad -1.3 %, cfg3 grad -2.7 %, cfg4 W* neutral): the long blur and
+    // the long analysis launches do better without early launch (their CTAs, pre-placed while the
+    // previous kernel drains, cost that kernel's tail more than they save)
+    const char *e = getenv("WL_NO_PDL");
+    return e ? e : "bA";
+  }();
+  return strchr(off, kind) == nullptr;
 }
 
 int short_run_max(int dflt) {

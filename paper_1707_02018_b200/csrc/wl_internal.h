@@ -139,11 +139,15 @@ cudaError_t kernel_resident(const void *kern, int nt, size_t smem, long long *re
 // synthesis 2 on B200); WL_SHORT_MAX overrides both (0 disables; A/B switch).
 int short_run_max(int dflt);
 
+// PDL per launch site: kind 'A' / 'a' (analysis, long / short runs), 'S' / 's' (synthesis), 'b'
+// (blur).  WL_NO_PDL lists the kinds launched without it (an A/B switch; "AasSb" = none).
+bool pdl_enabled(char kind);
+
 // Launch with programmatic stream serialization (PDL): the kernel may start while the
 // previous kernel of the stream drains; it must call pdl_wait() before its first global
 // memory access (every streaming kernel of libwl does, right after its shared-memory setup).
 template <typename Kern, typename Params>
-cudaError_t launch_pdl(Kern kern, int grid, int nt, size_t smem, cudaStream_t s, const Params &p) {
+cudaError_t launch_pdl(Kern kern, int grid, int nt, size_t smem, cudaStream_t s, const Params &p, char kind) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3((unsigned)nt);
@@ -153,7 +157,7 @@ cudaError_t launch_pdl(Kern kern, int grid, int nt, size_t smem, cudaStream_t s,
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled(kind) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
