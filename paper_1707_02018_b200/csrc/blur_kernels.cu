@@ -38,6 +38,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 
@@ -270,6 +271,11 @@ __global__ void __launch_bounds__(BCfg<T, HW, RESID>::NT, sizeof(T) == 4 ? (BCfg
     const int img = col / p.nstrips, strip = col - img * p.nstrips;
     if (r0 >= r1) continue;  // (uniform) empty trailing band
     const int c0 = strip * C::TW;
+    // interior strips (the u window and every output inside the image, 16-byte rows) run a copy
+    // of the body without the per-item edge and column guards
+    const bool interior = p.fast && c0 - C::A >= 0 && c0 + C::TW + C::A <= p.w;
+    auto run_body = [&](auto edge_tag) {
+    constexpr bool EDGE = decltype(edge_tag)::value;
     const T *u = p.u + (long long)img * p.h * p.w;
     const T *bimg = RESID ? p.b + (long long)img * p.h * p.w : nullptr;
     T *out = p.out + (long long)img * p.h * p.w;
@@ -279,22 +285,22 @@ __global__ void __launch_bounds__(BCfg<T, HW, RESID>::NT, sizeof(T) == 4 ? (BCfg
 
     // per-run item facts: skip items whose outputs are all outside the image (never read)
     const int oB = c0 - C::HB + C::V * segB;  // image column of B's first output
-    const bool actB = actB0 && oB < p.w && oB + C::V > 0;
+    const bool actB = actB0 && (!EDGE || (oB < p.w && oB + C::V > 0));
     const int gB = c0 - C::A + C::V * segB;   // image column of B's window start
-    const bool edgeB = gB < 0 || gB + C::NW1 > p.w;
+    const bool edgeB = EDGE && (gB < 0 || gB + C::NW1 > p.w);
     const int colC = RESID ? c0 - C::HB + 2 * mC : c0 + 2 * mC;  // image column of C's pair
-    const bool actC = actC0 && colC < p.w && colC + 2 > 0;
-    const bool ovecC = p.fast && colC + 1 < p.w;
+    const bool actC = actC0 && (!EDGE || (colC < p.w && colC + 2 > 0));
+    const bool ovecC = !EDGE || (p.fast && colC + 1 < p.w);
     P fmask;  // f counts each in-image pixel of the tile once
     fmask.x = (colC >= c0 && colC < c0 + C::TW && colC < p.w) ? T(1) : T(0);
     fmask.y = (colC + 1 >= c0 && colC + 1 < c0 + C::TW && colC + 1 < p.w) ? T(1) : T(0);
     const int oH = c0 + C::V * segH;
-    const bool actH = actH0 && oH < p.w;
+    const bool actH = actH0 && (!EDGE || oH < p.w);
     const int gH = c0 - C::HB + C::V * segH;  // image column of H2's window start
-    const bool edgeH = gH < 0 || gH + C::NW2 > p.w;
+    const bool edgeH = EDGE && (gH < 0 || gH + C::NW2 > p.w);
     const int colD = c0 + 2 * mD;
-    const bool actD = actD0 && colD < p.w;
-    const bool ovecD = p.fast && colD + 1 < p.w;
+    const bool actD = actD0 && (!EDGE || colD < p.w);
+    const bool ovecD = !EDGE || (p.fast && colD + 1 < p.w);
     double fsx = 0.0, fsy = 0.0;  // per-column sums of r^2 (masked to the tile at the end)
 
     // batch k: u rows e_begin + kG .. and (residual) b rows e_begin + kG - HW .. -> slot k & 1.
@@ -465,6 +471,9 @@ __global__ void __launch_bounds__(BCfg<T, HW, RESID>::NT, sizeof(T) == 4 ? (BCfg
         atomicAdd(p.f + img, 0.5 * s);
       }
     }
+    };
+    if (interior) run_body(std::false_type{});
+    else run_body(std::true_type{});
   }
 }
 
