@@ -70,8 +70,16 @@ struct BCfg {
 #define WL_BLUR_G 16
 #endif
   static constexpr int G = (2 * HW > WL_BLUR_G) ? 32 : WL_BLUR_G;
-  static constexpr int V = 8;                               // outputs per item, horizontal passes
-  static constexpr int VC = 4;                              // output rows per item, vertical passes
+#ifndef WL_BLUR_V
+#define WL_BLUR_V 8
+#endif
+#ifndef WL_BLUR_VC
+#define WL_BLUR_VC 4
+#endif
+  static constexpr int HB_ = RESID ? round_up_c(HW, 4) : 0;
+  static constexpr int VR = sizeof(T) == 4 ? WL_BLUR_V : 8;
+  static constexpr int V = ((TW + 2 * HB_) % VR == 0 && TW % VR == 0) ? VR : 8;  // outputs per item, horizontal passes
+  static constexpr int VC = sizeof(T) == 4 ? WL_BLUR_VC : 4;  // output rows per item, vertical passes
   static constexpr int HB = RESID ? round_up_c(HW, 4) : 0;  // r columns beyond the tile per side
   static constexpr int NH1 = TW + 2 * HB;                   // columns of h1 / r
   static constexpr int A = round_up_c(HB + HW, VEC);        // u columns loaded beyond the tile per side
@@ -88,8 +96,8 @@ struct BCfg {
   static constexpr int HR = 2 * HW + G;                     // rows of a history buffer
   static_assert(2 * HW <= G, "history move must not overlap");
   static_assert(NH1 % V == 0 && TW % V == 0, "segments");
-  static_assert(8 * (NH1 / V - 1) + NW1 <= UW, "pass B window overruns the u row");
-  static_assert(!RESID || 8 * (TW / V - 1) + NW2 <= NH1, "pass H2 window overruns the r row");
+  static_assert(V * (NH1 / V - 1) + NW1 <= UW, "pass B window overruns the u row");
+  static_assert(!RESID || V * (TW / V - 1) + NW2 <= NH1, "pass H2 window overruns the r row");
   static constexpr int SEG1 = NH1 / V, SEG2 = TW / V;
   static constexpr int ITEMS_B = SEG1 * G;
   static constexpr int ITEMS_C = (RESID ? NH1 / 2 : TW / 2) * (G / VC);
