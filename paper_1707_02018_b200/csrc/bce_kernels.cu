@@ -25,7 +25,10 @@
 namespace wl {
 namespace {
 
-constexpr int BV = 8;     // outputs per thread item
+#ifndef WL_BCE_BV
+#define WL_BCE_BV 8
+#endif
+constexpr int BV = WL_BCE_BV;  // outputs per thread item
 constexpr int BNT = 256;  // threads per CTA
 
 __host__ __device__ constexpr int rup(int v, int a) { return (v + a - 1) / a * a; }
