@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? 768 /
 #pragma unroll
         for (int k = 0; k < V; k++) acc[k] = zero2<P>();
 #pragma unroll
-        for (int j = 0; j < L; j++) {  // tap-outer
+        for (int j = L - 1; j >= 0; j--) {  // tap-outer, lowest window samples first (earliest loads)
           const P f = p.fb[j];
 #pragma unroll
           for (int k = 0; k < V; k++) acc[k] = fma2(f, splat2<P>(win[C::SHIFT + 2 * k + L - 1 - j]), acc[k]);
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? 768 /
 #pragma unroll
         for (int v = 0; v < VC; v++) a0[v] = a1[v] = zero2<P>();
 #pragma unroll
-        for (int j = 0; j < L; j++) {
+        for (int j = L - 1; j >= 0; j--) {
           const P fl = p.slo[j], fh = p.shi[j];
 #pragma unroll
           for (int v = 0; v < VC; v++) {
