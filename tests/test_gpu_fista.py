@@ -163,3 +163,29 @@ def test_fista_graph_replay_matches_eager(torch, dtype, tol):
     assert tg == pytest.approx(te, rel=1e-14)
     assert float((xg - xe).abs().max()) <= tol * max(float(xe.abs().max()), 1e-30)
     assert float((yg - ye).abs().max()) <= tol * max(float(ye.abs().max()), 1e-30)
+
+
+def test_cfg5_fused_fista_step_full_size(torch):
+    """One fused FISTA step at the bench configuration (cfg5: 4 x 4096^2 CDF 9/7, 5 levels,
+    symmetric, fp32), device-resident t, replayed as a CUDA graph like bench.py's FISTA line,
+    against the oracle's grad + update."""
+    c = inputs.CONFIGS[5]
+    plan = wl.Plan(c.h, c.w, c.levels, c.filt, c.bc, c.dtype)
+    blur = wl.Blur(c.h, c.w, inputs.BLUR_NTAPS, inputs.BLUR_SIGMA, dtype=c.dtype)
+    x, y, bl, nz = inputs.workload(c, plan.p_valid)
+    x = inputs.cast(x, c.dtype)
+    y0 = inputs.cast(inputs.coefficients(np.random.default_rng(3), c.batch, plan.p_valid, 0.05), c.dtype)
+    b = inputs.cast(O.blur(bl) + nz, c.dtype)
+    xd = dev(torch, plan.from_packed(x), c.dtype)
+    yd = dev(torch, plan.from_packed(y0), c.dtype)
+    bd = dev(torch, b, c.dtype)
+    t_dev = torch.full((1,), 2.0, dtype=torch.float64, device="cuda")
+    ws = plan._ws(wl.OP_FISTA, c.batch, blur=blur)
+    graph = wl.Graph(lambda: wl.fista_step(plan, blur, bd, xd, yd, t_dev, 1e-3, 1.1, ws=ws), warmup=0)
+    graph.replay()
+    torch.cuda.synchronize()
+    g, _ = O.grad(y0.astype(np.float64), b.astype(np.float64), c.levels, c.filt, c.bc)
+    xo, yo, to = O.fista_update(g, x.astype(np.float64), y0.astype(np.float64), 2.0, 1e-3, 1.1)
+    assert float(t_dev.item()) == pytest.approx(to, rel=1e-15)
+    assert rel(plan.to_packed(xd.double().cpu().numpy()), xo) <= 2e-6
+    assert rel(plan.to_packed(yd.double().cpu().numpy()), yo) <= 2e-6
