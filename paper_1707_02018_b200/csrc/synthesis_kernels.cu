@@ -47,8 +47,8 @@ struct SCfg {
 #endif
   static constexpr int G = WL_SYN_G;                     // coefficient rows per iteration
 #ifndef WL_SYN_SP
-#define WL_SYN_SP 8
-#endif
+#define WL_SYN_SP 4  // A/B on B200: 4 output column pairs per S1 item (S1 then uses all 256 threads) beat 8
+#endif                // by 11 % at cfg5 and 8 % at cfg4
 #ifndef WL_SYN_VC
 #define WL_SYN_VC 4
 #endif
