@@ -64,7 +64,10 @@ struct BCfg {
   using P = typename Pair<T>::t;
   static constexpr int VEC = Vec16<T>::n;
   // output columns per strip: the residual frame NH1 = TW + 2HB is a multiple of the 16-item warps
-  static constexpr int TW = sizeof(T) == 4 ? (RESID ? 112 : 128) : (RESID ? 48 : 64);
+#ifndef WL_BLUR_TWR
+#define WL_BLUR_TWR 112
+#endif
+  static constexpr int TW = sizeof(T) == 4 ? (RESID ? WL_BLUR_TWR : 128) : (RESID ? 48 : 64);
   // extended rows per iteration; G >= 2HW keeps the history move [G, G+2HW) -> [0, 2HW) non-overlapping
 #ifndef WL_BLUR_G
 #define WL_BLUR_G 16
