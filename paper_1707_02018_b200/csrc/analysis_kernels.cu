@@ -74,12 +74,18 @@ struct ACfg {
 #endif
   static constexpr bool F32 = sizeof(T) == 4;
   static constexpr int TQ = F32 ? WL_ANA_TQ : 32;                     // coefficient columns per strip
-  static constexpr int G = (F32 && !FU_) ? WL_ANA_G : 8;              // coefficient rows per iteration
+#ifndef WL_ANA_SHORT_SMALL
+#define WL_ANA_SHORT_SMALL 1
+#endif
+  // the small tile (8 rows per iteration): the fused FISTA variant, and the short-run variant for
+  // filters shorter than db8 (A/B on B200: cfg2 W* -18 %, cfg3 -2 %, cfg5 -1 %; db8 +4 %, so not there)
+  static constexpr bool SMALL = FU_ || (WL_ANA_SHORT_SMALL && NS_ == 4 && L < 16);
+  static constexpr int G = (F32 && !SMALL) ? WL_ANA_G : 8;              // coefficient rows per iteration
   static constexpr int GI = 2 * G;                       // input rows per iteration
-  static constexpr int V = (F32 && !FU_) ? WL_ANA_V : 8;      // coefficient outputs per B item
+  static constexpr int V = (F32 && !SMALL) ? WL_ANA_V : 8;    // coefficient outputs per B item
   // coefficient rows per C item: the 16-tap db8 window (2 VC + 14 history rows) does better with
   // 4 (cfg4 W* -3.6 %), the shorter filters with 8
-  static constexpr int VC = (F32 && !FU_) ? (L >= 16 ? 4 : WL_ANA_VC) : 4;
+  static constexpr int VC = (F32 && !SMALL) ? (L >= 16 ? 4 : WL_ANA_VC) : 4;
   static constexpr int SHIFT = ((2 - L) % VEC + VEC) % VEC;  // box column of input column 2q0+2-L
   static constexpr int UW = round_up_c(SHIFT + 2 * TQ + L - 2, VEC);  // input box width
   static constexpr int UP = UW;                          // dense TMA box rows
@@ -413,11 +419,12 @@ cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
   p.m1 = a.m1;
   p.ext = a.ext;
   p.fast = (a.in_pitch % C::VEC == 0) && (a.in_bstride % C::VEC == 0) && (reinterpret_cast<uintptr_t>(a.in) % 16 == 0);
-  bool tma = p.fast && !getenv("WL_NO_TMA") && a.ext != EXT_SYM_PADJ;
-  if (tma)
-    tma = encode_tmap_3d(&p.tmap, sizeof(T), a.in, (uint64_t)a.n1, (uint64_t)a.n0, (uint64_t)a.batch,
-                         (uint64_t)a.in_pitch * sizeof(T), (uint64_t)a.in_bstride * sizeof(T), C::UW, C::GI);
-  p.tma = tma;
+  const bool tma_ok = p.fast && !getenv("WL_NO_TMA") && a.ext != EXT_SYM_PADJ;
+  // the tensor map's box is the launched configuration's input block (UW columns x GI rows)
+  auto encode = [&](int uw, int gi) {
+    p.tma = tma_ok && encode_tmap_3d(&p.tmap, sizeof(T), a.in, (uint64_t)a.n1, (uint64_t)a.n0, (uint64_t)a.batch,
+                                     (uint64_t)a.in_pitch * sizeof(T), (uint64_t)a.in_bstride * sizeof(T), uw, gi);
+  };
   p.tma_any_block = a.ext == EXT_ZERO;  // TMA's zero fill is the zero extension
   for (int j = 0; j < L; j++) {
     p.flo[j] = T(a.lo[j]);
@@ -446,10 +453,12 @@ cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
     e = kernel_resident(reinterpret_cast<const void *>(k_ana_stream<T, L, FU, 4>), C4::NT, C4::smem_bytes(FU),
                         &resident);
     if (e != cudaSuccess) return e;
-    p.runs = RunMap::make((long long)a.batch * p.nstrips, a.m0, resident, C::G, 1);
+    p.runs = RunMap::make((long long)a.batch * p.nstrips, a.m0, resident, C4::G, 1);
+    encode(C4::UW, C4::GI);
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
     e = launch_pdl(k_ana_stream<T, L, FU, 4>, grid, C4::NT, C4::smem_bytes(FU), s, p, 'a');
   } else {
+    encode(C::UW, C::GI);
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
     e = launch_pdl(k_ana_stream<T, L, FU, 0>, grid, C::NT, C::smem_bytes(FU), s, p, 'A');
   }
