@@ -45,7 +45,11 @@ struct SCfg {
 #ifndef WL_SYN_G
 #define WL_SYN_G 16
 #endif
-  static constexpr int G = WL_SYN_G;                     // coefficient rows per iteration
+#ifndef WL_SYN_SHORT_G
+#define WL_SYN_SHORT_G 0
+#endif
+  // coefficient rows per iteration (short runs: WL_SYN_SHORT_G if set, A/B)
+  static constexpr int G = (NS_ == 4 && WL_SYN_SHORT_G > 0) ? WL_SYN_SHORT_G : WL_SYN_G;
 #ifndef WL_SYN_SP
 #define WL_SYN_SP 4  // A/B on B200: 4 output column pairs per S1 item (S1 then uses all 256 threads) beat 8
 #endif                // by 11 % at cfg5 and 8 % at cfg4
@@ -328,16 +332,20 @@ cudaError_t launch_synth_stream_t(const SynthesisArgs &a, cudaStream_t s) {
   static_assert(C::H <= H_MAX, "H_MAX");
   SynStreamParams<T, L> p;
   memset(&p, 0, sizeof p);
-  bool tma = !a.coef_mod && !getenv("WL_NO_TMA");  // WL_NO_TMA: debugging / A-B switch
+  const bool tma_ok = !a.coef_mod && !getenv("WL_NO_TMA");  // WL_NO_TMA: debugging / A-B switch
   for (int i = 0; i < 4; i++) {
     p.in[i] = static_cast<const T *>(a.in[i]);
     p.in_pitch[i] = a.in_pitch[i];
     p.in_bstride[i] = a.in_bstride[i];
-    if (tma)
-      tma = encode_tmap_3d(&p.tmap[i], sizeof(T), a.in[i], (uint64_t)a.m1, (uint64_t)a.m0, (uint64_t)a.batch,
-                           (uint64_t)a.in_pitch[i] * sizeof(T), (uint64_t)a.in_bstride[i] * sizeof(T), C::KCW, C::G);
   }
-  p.tma = tma;
+  // the tensor maps' box is the launched configuration's coefficient window (KCW x G)
+  auto encode = [&](int kcw, int g) {
+    bool tma = tma_ok;
+    for (int i = 0; i < 4 && tma; i++)
+      tma = encode_tmap_3d(&p.tmap[i], sizeof(T), a.in[i], (uint64_t)a.m1, (uint64_t)a.m0, (uint64_t)a.batch,
+                           (uint64_t)a.in_pitch[i] * sizeof(T), (uint64_t)a.in_bstride[i] * sizeof(T), kcw, g);
+    p.tma = tma;
+  };
   p.out = static_cast<T *>(a.out);
   p.out_pitch = a.out_pitch;
   p.out_bstride = a.out_bstride;
@@ -372,10 +380,12 @@ cudaError_t launch_synth_stream_t(const SynthesisArgs &a, cudaStream_t s) {
     e = kernel_resident(reinterpret_cast<const void *>(k_synth_stream<T, L, 4>), C4::NT, C4::smem_bytes(),
                         &resident);
     if (e != cudaSuccess) return e;
-    p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident, 2 * C::G, 2);
+    p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident, 2 * C4::G, 2);
+    encode(C4::KCW, C4::G);
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
     e = launch_pdl(k_synth_stream<T, L, 4>, grid, C4::NT, C4::smem_bytes(), s, p, 's');
   } else {
+    encode(C::KCW, C::G);
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
     e = launch_pdl(k_synth_stream<T, L, 0>, grid, C::NT, C::smem_bytes(), s, p, 'S');
   }
