@@ -297,6 +297,28 @@ def run_wl(args):
              "config": "cfg5, lambda 1e-3, L 1"}
     del xf, yf, wsf
 
+    # ---- W, W*, W-dagger at every other BASELINE config ("W and W-dagger rows for every
+    # config"), graph-replayed, algorithmic bytes es*B*(N + p) per operator
+    per_cfg = {}
+    for ci in (1, 2, 3, 4):
+        cc = inputs.CONFIGS[ci]
+        pc = wl.Plan(cc.h, cc.w, cc.levels, cc.filt, cc.bc, cc.dtype)
+        td = pc.torch_dtype
+        gen = torch.Generator(dev).manual_seed(ci)
+        imc = torch.randn(cc.batch, cc.h, cc.w, device=dev, dtype=td, generator=gen)
+        xc = pc.from_packed(torch.randn(cc.batch, pc.p_valid, device=dev, dtype=td, generator=gen))
+        oxc, oic = torch.empty_like(xc), torch.empty_like(imc)
+        wss = {op: pc._ws(op, cc.batch) for op in (wl.OP_SYNTHESIZE, wl.OP_ADJOINT, wl.OP_ANALYZE)}
+        nb = td.itemsize * cc.batch * (cc.h * cc.w + pc.p_valid)
+        row = {"config": f"{cc.batch}x{cc.h}x{cc.w} {cc.filt} {cc.bc} J={cc.levels} {cc.dtype}", "bytes": nb}
+        for name, fn in (("W", lambda: pc.synthesize(xc, out=oic, ws=wss[wl.OP_SYNTHESIZE])),
+                         ("W*", lambda: pc.adjoint(imc, out=oxc, ws=wss[wl.OP_ADJOINT])),
+                         ("W-dagger", lambda: pc.analyze(imc, out=oxc, ws=wss[wl.OP_ANALYZE]))):
+            tt = time_calls(torch, wl.Graph(fn).replay, 20)
+            row[name] = {"us": tt * 1e3, "GB/s": nb / (tt * 1e-3) / 1e9, "frac": nb / (tt * 1e-3) / 1e9 / hbm_peak}
+        per_cfg[f"cfg{ci}"] = row
+        del imc, xc, oxc, oic, wss
+
     # ---- Example 2: fused Eq. (6) gradient, paper sizes, 4096 random starts
     bc = inputs.BCE
     P_bce, C_b, K_b, N_b = 4096, bc["channels"], bc["K_est"], bc["N_est"]
@@ -361,7 +383,7 @@ def run_wl(args):
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(), "step_launch": "eager" if graph is None else "cuda_graph",
                 "ms_per_step_eager": ms_eager, "grad_evals_per_s": ws / (ms * 1e-3), "images_per_s": ws * B / (ms * 1e-3),
-                "grad_frac_of_hbm_roofline": value / ws / hbm_peak, "wstar_cfg4": wstar, "fista_cfg5": fista, "bce": bce, "kernels": kernels}
+                "grad_frac_of_hbm_roofline": value / ws / hbm_peak, "wstar_cfg4": wstar, "fista_cfg5": fista, "bce": bce, "operators_by_config": per_cfg, "kernels": kernels}
         print(json.dumps(line))
     if ws > 1:
         import torch.distributed as dist

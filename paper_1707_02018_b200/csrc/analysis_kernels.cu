@@ -205,6 +205,13 @@ __global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? 768 /
     const int q0 = strip * TQ;
     const int cbox = 2 * q0 + 2 - L - C::SHIFT;  // input column of box column 0 (VEC aligned)
     const T *in = p.in + (long long)img * p.in_bstride;
+    const bool cols_in = cbox >= 0 && cbox + C::UW <= p.n1;
+    // outside columns a stored output reads: [cbox, 0) and [n1, min(cbox + UW, 2 m1)); sym_fix needs
+    // their mirror images inside the box
+    const int fix_lim = min(cbox + C::UW, 2 * p.m1);
+    const int fix_nl = max(0, min(-cbox, C::UW)), fix_r0 = max(p.n1, cbox), fix_nr = max(0, fix_lim - fix_r0);
+    const bool sym_fix = p.ext == EXT_SYM && !cols_in && (cbox >= 0 || -2 * cbox - 1 < C::UW) &&
+                         (fix_nr == 0 || 2 * p.n1 - fix_lim >= cbox);
     const int nblk = (kr1 - kr0 + G - 1) / G;
     // C output columns q = q0 + 2 mC (+1) of subbands (setC: LL/HL from lo, LH/HH from hi)
     const int qc = q0 + 2 * mC;
@@ -230,8 +237,10 @@ __global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? 768 /
           cp_async16(fdst + ((band * 2 + arr) * G + r) * TQ + c * VEC, src);
         }
       }
-      const bool inside = r_in >= 0 && r_in + GI <= p.n0 && cbox >= 0 && cbox + C::UW <= p.n1;
-      if (p.tma && (p.tma_any_block || inside)) {
+      const bool rows_in = r_in >= 0 && r_in + GI <= p.n0;
+      // symmetric edge strips: the box still comes by TMA (zero fill outside) and the outside
+      // columns are mirrored inside shared memory after it lands (sym_fix)
+      if (p.tma && (p.tma_any_block || (rows_in && (cols_in || sym_fix)))) {
         if (tid == 0) {
           fence_proxy_async();
           mbar_arrive_expect_tx(bar + sl, GI * C::UW * sizeof(T));
@@ -245,7 +254,9 @@ __global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? 768 /
         const int sr = ext_src<T>(r_in + r, p.n0, p.ext, L - 1, wr);
         T *dst = dst0 + r * C::UP + v * VEC;
         const int cg = cbox + v * VEC;
-        if (sr < 0) {
+        // extended positions t >= 2m feed no stored output (out[k] reads t = 2k+1-j <= 2m-1): the
+        // window of a partial last strip / band is zero-filled there instead of gathered
+        if (sr < 0 || cg >= 2 * p.m1 || r_in + r >= 2 * p.m0) {
           T z[VEC];
 #pragma unroll
           for (int u = 0; u < VEC; u++) z[u] = T(0);
@@ -281,6 +292,20 @@ __global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? 768 /
         phase ^= 1u << slot;
       }
       __syncthreads();  // (1) block it landed; the history move of it-1 is done
+      if (sym_fix && p.tma) {
+        const int r_it = 2 * (kr0 + it * G);
+        if (r_it >= 0 && r_it + GI <= p.n0) {  // block it came by TMA: mirror its outside columns
+          T *ub = ubuf + slot * GI * C::UP;
+          const int per = fix_nl + fix_nr;
+          for (int idx = tid; idx < GI * per; idx += C::NT) {
+            const int r = idx / per, k = idx - r * per;
+            const int g = k < fix_nl ? cbox + k : fix_r0 + (k - fix_nl);
+            const int src = g < 0 ? -1 - g : 2 * p.n1 - 1 - g;
+            ub[r * C::UP + (g - cbox)] = ub[r * C::UP + (src - cbox)];
+          }
+          __syncthreads();
+        }
+      }
       {
         const int nb = it + C::NS - 1;  // its slot held block it-1, consumed before (1)
         armed &= ~(1u << (nb + 1) % C::NS);
