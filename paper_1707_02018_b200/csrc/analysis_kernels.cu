@@ -205,7 +205,8 @@ __global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? 768 /
     const int q0 = strip * TQ;
     const int cbox = 2 * q0 + 2 - L - C::SHIFT;  // input column of box column 0 (VEC aligned)
     const T *in = p.in + (long long)img * p.in_bstride;
-    const bool cols_in = cbox >= 0 && cbox + C::UW <= p.n1;
+    const int wpc = p.ext == EXT_SYM_PADJ ? L - 1 : 0;  // weighted edge columns (E_sym^dagger)*
+    const bool cols_in = cbox >= wpc && cbox + C::UW <= p.n1 - wpc;
     // outside columns a stored output reads: [cbox, 0) and [n1, min(cbox + UW, 2 m1)); sym_fix needs
     // their mirror images inside the box
     const int fix_lim = min(cbox + C::UW, 2 * p.m1);
@@ -237,7 +238,9 @@ __global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? 768 /
           cp_async16(fdst + ((band * 2 + arr) * G + r) * TQ + c * VEC, src);
         }
       }
-      const bool rows_in = r_in >= 0 && r_in + GI <= p.n0;
+      // (E_sym^dagger)*: TMA only where every row and column weight is 1 (L-1 inside the edges)
+      const int wpad = p.ext == EXT_SYM_PADJ ? L - 1 : 0;
+      const bool rows_in = r_in >= wpad && r_in + GI <= p.n0 - wpad;
       // symmetric edge strips: the box still comes by TMA (zero fill outside) and the outside
       // columns are mirrored inside shared memory after it lands (sym_fix)
       if (p.tma && (p.tma_any_block || (rows_in && (cols_in || sym_fix)))) {
@@ -261,8 +264,13 @@ __global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? 768 /
 #pragma unroll
           for (int u = 0; u < VEC; u++) z[u] = T(0);
           *reinterpret_cast<Vt *>(dst) = vec_make<T>(z);
-        } else if (p.fast && p.ext != EXT_SYM_PADJ && cg >= 0 && cg + VEC <= p.n1) {
+        } else if (p.fast && cg >= 0 && cg + VEC <= p.n1 &&
+                   (p.ext != EXT_SYM_PADJ || (wr == T(1) && cg >= L - 1 && cg + VEC <= p.n1 - (L - 1)))) {
+          // a plain 16-byte copy (for the weighted (E_sym^dagger)* extension only where every weight is 1)
           cp_async16(dst, in + (long long)sr * p.in_pitch + cg);
+        } else if (p.fast && p.ext == EXT_PER && p.n1 % VEC == 0 && ((cg % p.n1) + p.n1) % p.n1 + VEC <= p.n1) {
+          // periodic wrap of a whole aligned chunk (n1 is a multiple of VEC when p.fast)
+          cp_async16(dst, in + (long long)sr * p.in_pitch + ((cg % p.n1) + p.n1) % p.n1);
         } else {
           T z[VEC];
 #pragma unroll
@@ -444,7 +452,7 @@ cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
   p.m1 = a.m1;
   p.ext = a.ext;
   p.fast = (a.in_pitch % C::VEC == 0) && (a.in_bstride % C::VEC == 0) && (reinterpret_cast<uintptr_t>(a.in) % 16 == 0);
-  const bool tma_ok = p.fast && !getenv("WL_NO_TMA") && a.ext != EXT_SYM_PADJ;
+  const bool tma_ok = p.fast && !getenv("WL_NO_TMA");
   // the tensor map's box is the launched configuration's input block (UW columns x GI rows)
   auto encode = [&](int uw, int gi) {
     p.tma = tma_ok && encode_tmap_3d(&p.tmap, sizeof(T), a.in, (uint64_t)a.n1, (uint64_t)a.n0, (uint64_t)a.batch,

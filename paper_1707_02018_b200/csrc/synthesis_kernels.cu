@@ -175,6 +175,8 @@ __global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 768 / SCfg<T,
         const T *row = p.in[bnd] + (long long)img * p.in_bstride[bnd] + (long long)krr * p.in_pitch[bnd];
         if (row_ok && cg >= 0 && cg + VEC <= p.m1 && ((cg & (VEC - 1)) == 0)) {
           cp_async16(dst, row + cg);
+        } else if (p.coef_mod && p.m1 % VEC == 0 && (cg & (VEC - 1)) == 0 && ((cg % p.m1) + p.m1) % p.m1 + VEC <= p.m1) {
+          cp_async16(dst, row + ((cg % p.m1) + p.m1) % p.m1);  // periodic wrap of a whole aligned chunk
         } else {
           T z[VEC];
 #pragma unroll
