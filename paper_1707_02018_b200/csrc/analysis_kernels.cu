@@ -211,8 +211,8 @@ __global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? 768 /
     // their mirror images inside the box
     const int fix_lim = min(cbox + C::UW, 2 * p.m1);
     const int fix_nl = max(0, min(-cbox, C::UW)), fix_r0 = max(p.n1, cbox), fix_nr = max(0, fix_lim - fix_r0);
-    const bool sym_fix = p.ext == EXT_SYM && !cols_in && (cbox >= 0 || -2 * cbox - 1 < C::UW) &&
-                         (fix_nr == 0 || 2 * p.n1 - fix_lim >= cbox);
+    const bool sym_fix = (p.ext == EXT_SYM || p.ext == EXT_SYM_PADJ) && !cols_in &&
+                         (cbox >= 0 || -2 * cbox - 1 < C::UW) && (fix_nr == 0 || 2 * p.n1 - fix_lim >= cbox);
     const int nblk = (kr1 - kr0 + G - 1) / G;
     // C output columns q = q0 + 2 mC (+1) of subbands (setC: LL/HL from lo, LH/HH from hi)
     const int qc = q0 + 2 * mC;
@@ -302,7 +302,8 @@ __global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? 768 /
       __syncthreads();  // (1) block it landed; the history move of it-1 is done
       if (sym_fix && p.tma) {
         const int r_it = 2 * (kr0 + it * G);
-        if (r_it >= 0 && r_it + GI <= p.n0) {  // block it came by TMA: mirror its outside columns
+        const int wpad = p.ext == EXT_SYM_PADJ ? L - 1 : 0;
+        if (r_it >= wpad && r_it + GI <= p.n0 - wpad) {  // block it came by TMA: mirror its outside columns
           T *ub = ubuf + slot * GI * C::UP;
           const int per = fix_nl + fix_nr;
           for (int idx = tid; idx < GI * per; idx += C::NT) {
@@ -312,6 +313,23 @@ __global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? 768 /
             ub[r * C::UP + (g - cbox)] = ub[r * C::UP + (src - cbox)];
           }
           __syncthreads();
+          if (p.ext == EXT_SYM_PADJ) {
+            // (E_sym^dagger)* = E_sym diag(1/c): every column within L-1 of an edge, inside or
+            // mirrored, times 1/c of its source (c = 1 + [s < L-1] + [s >= n-L+1]); rows are all
+            // weight 1 here
+            const int Lp = L - 1;
+            const int la = cbox, lb = min(Lp, cbox + C::UW);               // left set [la, lb)
+            const int ra = max(cbox, p.n1 - Lp), rb = fix_lim;             // right set [ra, rb)
+            const int nl = max(0, lb - la), nr = max(0, rb - ra), per2 = nl + nr;
+            for (int idx = tid; idx < GI * per2; idx += C::NT) {
+              const int r = idx / per2, k = idx - r * per2;
+              const int g = k < nl ? la + k : ra + (k - nl);
+              const int src = g < 0 ? -1 - g : (g >= p.n1 ? 2 * p.n1 - 1 - g : g);
+              const int c = 1 + (src < Lp ? 1 : 0) + (src >= p.n1 - Lp ? 1 : 0);
+              if (c > 1) ub[r * C::UP + (g - cbox)] *= T(1) / T(c);
+            }
+            __syncthreads();
+          }
         }
       }
       {
