@@ -1,3 +1,5 @@
+#!/usr/bin/env python
+"""W*, W, W-dagger under every boundary condition at the cfg3 shape (8 x 2048^2), CUDA-graph replay."""
 import os, sys, torch, json
 sys.path.insert(0, os.getcwd())
 from paper_1707_02018_b200 import wl
