@@ -527,8 +527,11 @@ cudaError_t launch_stream(const BlurArgs &a, cudaStream_t s) {
   long long resident = 0;
   cudaError_t e = kernel_resident(reinterpret_cast<const void *>(kern), C::NT, smem, &resident);
   if (e != cudaSuccess) return e;
-  // one run per resident CTA when the columns allow it; every band >= 4 iterations
-  p.runs = RunMap::make((long long)a.batch * p.nstrips, (int)a.h, resident, 4 * C::G, 1);
+  // one run per resident CTA when the columns allow it; bands of >= G rows (small images need the CTAs)
+#ifndef WL_BLUR_MINROWS
+#define WL_BLUR_MINROWS 1  // in units of G; A/B on B200: 1 beat 4 (cfg2 grad -11 %, cfg1 -15 %, cfg3/5 equal)
+#endif
+  p.runs = RunMap::make((long long)a.batch * p.nstrips, (int)a.h, resident, WL_BLUR_MINROWS * C::G, 1);
   const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
   if (RESID && a.f) {
     e = cudaMemsetAsync(a.f, 0, sizeof(double) * (size_t)a.batch, s);
