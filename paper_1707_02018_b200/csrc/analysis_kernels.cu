@@ -451,6 +451,10 @@ __global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? 768 /
   }
 }
 
+#ifndef WL_ANA_MINROWS
+#define WL_ANA_MINROWS 1  // minimum band height in units of G/2 coefficient rows (A/B on B200: 1 beat 2, cfg4 W* -7 %)
+#endif
+
 template <typename T, int L, bool FU>
 cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
   using C = ACfg<T, L, 0, FU>;
@@ -497,14 +501,14 @@ cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
   cudaError_t e = kernel_resident(reinterpret_cast<const void *>(k_ana_stream<T, L, FU, 0>), C::NT,
                                   C::smem_bytes(FU), &resident);
   if (e != cudaSuccess) return e;
-  p.runs = RunMap::make((long long)a.batch * p.nstrips, a.m0, resident, C::G, 1);
+  p.runs = RunMap::make((long long)a.batch * p.nstrips, a.m0, resident, std::max(1, C::G * WL_ANA_MINROWS / 2), 1);
   const int band = (a.m0 + p.runs.nb_lo - 1) / p.runs.nb_lo;
   if ((band + C::G - 1) / C::G <= short_run_max(3)) {
     using C4 = ACfg<T, L, 4, FU>;
     e = kernel_resident(reinterpret_cast<const void *>(k_ana_stream<T, L, FU, 4>), C4::NT, C4::smem_bytes(FU),
                         &resident);
     if (e != cudaSuccess) return e;
-    p.runs = RunMap::make((long long)a.batch * p.nstrips, a.m0, resident, C4::G, 1);
+    p.runs = RunMap::make((long long)a.batch * p.nstrips, a.m0, resident, std::max(1, C4::G * WL_ANA_MINROWS / 2), 1);
     encode(C4::UW, C4::GI);
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
     e = launch_pdl(k_ana_stream<T, L, FU, 4>, grid, C4::NT, C4::smem_bytes(FU), s, p, 'a');

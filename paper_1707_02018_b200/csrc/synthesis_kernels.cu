@@ -328,6 +328,10 @@ __global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 768 / SCfg<T,
   }
 }
 
+#ifndef WL_SYN_MINROWS
+#define WL_SYN_MINROWS 1  // minimum band height in units of G output rows (A/B on B200: 1 beat 2 on every small config)
+#endif
+
 template <typename T, int L>
 cudaError_t launch_synth_stream_t(const SynthesisArgs &a, cudaStream_t s) {
   using C = SCfg<T, L>;
@@ -374,7 +378,7 @@ cudaError_t launch_synth_stream_t(const SynthesisArgs &a, cudaStream_t s) {
                                   &resident);
   if (e != cudaSuccess) return e;
   // one run per resident CTA when the columns allow it; even bands of >= 4 iterations
-  p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident, 2 * C::G, 2);
+  p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident, WL_SYN_MINROWS * C::G, 2);
   const int band = (span0 + p.runs.nb_lo - 1) / p.runs.nb_lo;
   if ((band / 2 + C::H - 1) / C::G + 1 <= short_run_max(2)) {
     // short runs (coarse levels): every batch of the run in flight at once
@@ -382,7 +386,7 @@ cudaError_t launch_synth_stream_t(const SynthesisArgs &a, cudaStream_t s) {
     e = kernel_resident(reinterpret_cast<const void *>(k_synth_stream<T, L, 4>), C4::NT, C4::smem_bytes(),
                         &resident);
     if (e != cudaSuccess) return e;
-    p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident, 2 * C4::G, 2);
+    p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident, WL_SYN_MINROWS * C4::G, 2);
     encode(C4::KCW, C4::G);
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
     e = launch_pdl(k_synth_stream<T, L, 4>, grid, C4::NT, C4::smem_bytes(), s, p, 's');
