@@ -474,7 +474,7 @@ cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
   p.m1 = a.m1;
   p.ext = a.ext;
   p.fast = (a.in_pitch % C::VEC == 0) && (a.in_bstride % C::VEC == 0) && (reinterpret_cast<uintptr_t>(a.in) % 16 == 0);
-  const bool tma_ok = p.fast && !getenv("WL_NO_TMA");
+  const bool tma_ok = p.fast && tma_enabled();
   // the tensor map's box is the launched configuration's input block (UW columns x GI rows)
   auto encode = [&](int uw, int gi) {
     p.tma = tma_ok && encode_tmap_3d(&p.tmap, sizeof(T), a.in, (uint64_t)a.n1, (uint64_t)a.n0, (uint64_t)a.batch,

@@ -338,7 +338,7 @@ cudaError_t launch_synth_stream_t(const SynthesisArgs &a, cudaStream_t s) {
   static_assert(C::H <= H_MAX, "H_MAX");
   SynStreamParams<T, L> p;
   memset(&p, 0, sizeof p);
-  const bool tma_ok = !a.coef_mod && !getenv("WL_NO_TMA");  // WL_NO_TMA: debugging / A-B switch
+  const bool tma_ok = !a.coef_mod && tma_enabled();  // WL_NO_TMA: debugging / A-B switch
   for (int i = 0; i < 4; i++) {
     p.in[i] = static_cast<const T *>(a.in[i]);
     p.in_pitch[i] = a.in_pitch[i];

@@ -66,6 +66,11 @@ bool encode_tmap_3d(void *map, int elem_bytes, const void *base, uint64_t d0, ui
   return true;
 }
 
+bool tma_enabled() {
+  static const bool v = getenv("WL_NO_TMA") == nullptr;
+  return v;
+}
+
 bool pdl_enabled(char kind) {
   static const char *off = [] {
     // measured on B200 (cfg5 grad -1.3 %, cfg3 grad -2.7 %, cfg4 W* neutral): the long blur and

@@ -139,6 +139,9 @@ cudaError_t kernel_resident(const void *kern, int nt, size_t smem, long long *re
 // synthesis 2 on B200); WL_SHORT_MAX overrides both (0 disables; A/B switch).
 int short_run_max(int dflt);
 
+// TMA loads unless WL_NO_TMA is set (debugging / A-B switch); read once per process
+bool tma_enabled();
+
 // PDL per launch site: kind 'A' / 'a' (analysis, long / short runs), 'S' / 's' (synthesis), 'b'
 // (blur).  WL_NO_PDL lists the kinds launched without it (an A/B switch; "AasSb" = none).
 bool pdl_enabled(char kind);
