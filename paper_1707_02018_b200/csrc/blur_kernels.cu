@@ -504,7 +504,7 @@ cudaError_t launch_stream(const BlurArgs &a, cudaStream_t s) {
               (reinterpret_cast<uintptr_t>(a.out) % 16 == 0);
   if (RESID) fast = fast && (reinterpret_cast<uintptr_t>(a.b) % 16 == 0);
   p.fast = fast;
-  bool tma = fast && a.h >= C::G && !getenv("WL_NO_TMA");  // WL_NO_TMA: debugging / A-B switch
+  bool tma = fast && a.h >= C::G && tma_enabled();  // WL_NO_TMA: debugging / A-B switch
   const uint64_t rs = (uint64_t)p.w * sizeof(T), is = rs * (uint64_t)p.h;
   if (tma) tma = encode_tmap_3d(&p.tmap_u, sizeof(T), a.in, p.w, p.h, a.batch, rs, is, C::UW, C::G);
   if (tma && RESID) tma = encode_tmap_3d(&p.tmap_b, sizeof(T), a.b, p.w, p.h, a.batch, rs, is, C::NH1, C::G);
