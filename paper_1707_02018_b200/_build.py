@@ -41,8 +41,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, lib
     """Compile every csrc source for sm_100a and link `lib` (defines: extra -D flags for A/B builds)."""
     os.makedirs(obj, exist_ok=True)
     hdr_t = max([_mtime(h) for h in _headers()] + [_mtime(__file__)])
-    objs = []
-    changed = force
+    objs, cmds = [], []
     for src in _sources():
         o = os.path.join(obj, os.path.basename(src) + ".o")
         objs.append(o)
@@ -52,8 +51,14 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, lib
                 cmd += ["-Xptxas", "-v"]
             if verbose:
                 print(" ".join(cmd), file=sys.stderr)
-            subprocess.check_call(cmd)
-            changed = True
+            cmds.append(cmd)
+    changed = force or bool(cmds)
+    # the translation units are independent: compile them concurrently (the template-heavy
+    # kernel files dominate, one process each)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        for _ in ex.map(subprocess.check_call, cmds):
+            pass
     if changed or _mtime(lib) < max(_mtime(o) for o in objs):
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib, *objs, "-lcuda"]
         if verbose:
