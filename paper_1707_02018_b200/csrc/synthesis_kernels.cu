@@ -150,7 +150,8 @@ __global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 768 / SCfg<T,
       const int kr = s_first + k * G;
       const int sl = k % C::NS;
       T *dst0 = cbuf + sl * 4 * C::BAND_ELEMS;
-      if (p.tma) {
+      // periodic plans: TMA only for windows that need no wrap (the zero fill is the crop otherwise)
+      if (p.tma && (!p.coef_mod || (kr >= 0 && kr + G <= p.m0 && kc0 >= 0 && kc0 + C::KCW <= p.m1))) {
         if (tid == 0) {
           fence_proxy_async();
           mbar_arrive_expect_tx(bar + sl, 4 * C::BAND_ELEMS * sizeof(T));
@@ -338,7 +339,7 @@ cudaError_t launch_synth_stream_t(const SynthesisArgs &a, cudaStream_t s) {
   static_assert(C::H <= H_MAX, "H_MAX");
   SynStreamParams<T, L> p;
   memset(&p, 0, sizeof p);
-  const bool tma_ok = !a.coef_mod && tma_enabled();  // WL_NO_TMA: debugging / A-B switch
+  const bool tma_ok = tma_enabled();  // WL_NO_TMA: debugging / A-B switch
   for (int i = 0; i < 4; i++) {
     p.in[i] = static_cast<const T *>(a.in[i]);
     p.in_pitch[i] = a.in_pitch[i];
