@@ -40,6 +40,7 @@ __device__ __forceinline__ int ext_src(int t, int n, int ext, int Lp, T &w) {
   w = T(1);
   if (ext == EXT_ZERO) return (t >= 0 && t < n) ? t : -1;
   if (ext == EXT_PER) {
+    if (t >= 0 && t < n) return t;  // the common case: no integer division
     int r = t % n;
     return r < 0 ? r + n : r;
   }

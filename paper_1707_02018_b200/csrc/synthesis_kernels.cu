@@ -168,16 +168,19 @@ __global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 768 / SCfg<T,
         T *dst = dst0 + bnd * C::BAND_ELEMS + r * C::KCP + v * VEC;
         bool row_ok = true;
         if (p.coef_mod) {
-          krr %= p.m0;
-          if (krr < 0) krr += p.m0;
+          if (krr < 0 || krr >= p.m0) {  // wrap (integer division only off the common path)
+            krr %= p.m0;
+            if (krr < 0) krr += p.m0;
+          }
         } else {
           row_ok = krr >= 0 && krr < p.m0;
         }
         const T *row = p.in[bnd] + (long long)img * p.in_bstride[bnd] + (long long)krr * p.in_pitch[bnd];
         if (row_ok && cg >= 0 && cg + VEC <= p.m1 && ((cg & (VEC - 1)) == 0)) {
           cp_async16(dst, row + cg);
-        } else if (p.coef_mod && p.m1 % VEC == 0 && (cg & (VEC - 1)) == 0 && ((cg % p.m1) + p.m1) % p.m1 + VEC <= p.m1) {
-          cp_async16(dst, row + ((cg % p.m1) + p.m1) % p.m1);  // periodic wrap of a whole aligned chunk
+        } else if (p.coef_mod && p.m1 % VEC == 0 && (cg & (VEC - 1)) == 0 && (cg >= -p.m1 && cg < 2 * p.m1) &&
+                   (cg < 0 ? cg + p.m1 : (cg >= p.m1 ? cg - p.m1 : cg)) + VEC <= p.m1) {
+          cp_async16(dst, row + (cg < 0 ? cg + p.m1 : (cg >= p.m1 ? cg - p.m1 : cg)));  // whole aligned wrapped chunk
         } else {
           T z[VEC];
 #pragma unroll
@@ -185,8 +188,10 @@ __global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 768 / SCfg<T,
             int c = cg + i;
             bool ok = row_ok;
             if (p.coef_mod) {
-              c %= p.m1;
-              if (c < 0) c += p.m1;
+              if (c < 0 || c >= p.m1) {
+                c %= p.m1;
+                if (c < 0) c += p.m1;
+              }
             } else {
               ok = ok && c >= 0 && c < p.m1;
             }
