@@ -121,3 +121,35 @@ def test_compute_calls_refuse_cpu_tensors():
     p = wl.Plan(32, 32, 2, "db2", "zero", "float32")
     with pytest.raises(ValueError):
         p.adjoint(torch.zeros(32, 32))
+
+
+def test_new_entry_points_validate_before_any_launch():
+    """The FISTA / host-buffer / adjoint-choice / Example 2 entry points reject bad arguments with a
+    status and a message before touching the device (so this runs without a GPU)."""
+    L = wl.lib()
+    p = wl.Plan(32, 32, 2, "db2", "symmetric", "float32")
+    b = wl.Blur(32, 32)
+    bad_blur = wl.Blur(32, 40)
+    vp = ctypes.c_void_p
+    assert L.wl_grad_adj(p._h, b._h, 1, vp(16), vp(32), vp(48), None, 7, None, None) == wl.WL_EINVAL
+    assert b"adj" in L.wl_last_error()
+    assert L.wl_grad_host(p._h, None, 1, vp(16), vp(32), vp(48), None, None, None) == wl.WL_EINVAL
+    assert L.wl_grad_host(p._h, bad_blur._h, 1, vp(16), vp(32), vp(48), None, None, None) == wl.WL_EINVAL
+    assert L.wl_grad_host(p._h, b._h, 1, None, vp(32), vp(48), None, None, None) == wl.WL_EINVAL
+    assert L.wl_grad_host(p._h, b._h, 0, None, None, None, None, None, None) == wl.WL_OK   # empty batch
+    assert L.wl_fista_step_dev(p._h, b._h, 1, vp(16), vp(32), vp(48), None, 0.1, 1.0, None, 0, None,
+                               None) == wl.WL_EINVAL
+    assert b"t_dev" in L.wl_last_error()
+    assert L.wl_fista_step(p._h, b._h, 1, vp(16), vp(32), vp(48), 0.5, 0.1, 1.0, None, 0, None,
+                           None) == wl.WL_EINVAL                                            # t < 1
+    assert L.wl_fista_update(p._h, 1, vp(16), vp(32), vp(48), 1.0, 0.1, 0.0, None) == wl.WL_EINVAL  # lip = 0
+    # Example 2
+    assert L.wl_bce_grad(0, 1, 2, 5, 9, vp(16), vp(32), vp(48), 0, 0.01, 0.0, vp(64), vp(80), None,
+                         None) == wl.WL_EINVAL                                              # delta = 0
+    assert L.wl_bce_grad(0, 1, 0, 5, 9, vp(16), vp(32), vp(48), 0, 0.01, 0.1, vp(64), vp(80), None,
+                         None) == wl.WL_EINVAL                                              # channels = 0
+    assert L.wl_bce_grad(0, 1, 2, 20000, 20000, vp(16), vp(32), vp(48), 0, 0.01, 0.1, vp(64), vp(80), None,
+                         None) == wl.WL_ESIZE                                               # shared memory
+    assert L.wl_conv_full(0, 1, 0, 9, vp(16), vp(32), vp(48), None) == wl.WL_ESIZE       # K = 0
+    assert L.wl_conv_full(5, 1, 3, 9, vp(16), vp(32), vp(48), None) == wl.WL_EDTYPE      # bad dtype
+    assert L.wl_conv_adjoint_h(0, 0, 3, 9, None, None, None, None) == wl.WL_OK           # empty batch
