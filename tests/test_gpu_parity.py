@@ -282,3 +282,25 @@ def test_multi_strip_shapes(torch, filt, bc, shape, dtype):
     assert rel(plan.to_packed(host(plan.adjoint(yd))), O.adjoint(y, J, filt, bc)) <= tol
     assert rel(plan.to_packed(host(plan.analyze(yd))), O.analyze(y, J, filt, bc)) <= tol
     assert rel(host(plan.analyze_adjoint(xd)), O.analyze_adjoint(x, h, w, J, filt, bc)) <= tol
+
+
+# -------------------------------------------------------------- extreme aspect ratios / many images
+@pytest.mark.parametrize("shape,B", [((16, 8192, 2), 1), ((8192, 24, 2), 1), ((40, 56, 3), 64)])
+@pytest.mark.parametrize("bc", ["symmetric", "zero", "symmetric_edag"])
+def test_extreme_shapes(torch, shape, B, bc):
+    h, w, J = shape
+    filt = "db4"
+    plan = wl.Plan(h, w, J, filt, bc, "float32")
+    blur = wl.Blur(h, w, 15, 3.0, dtype="float32") if min(h, w) >= 8 else None
+    rng = np.random.default_rng(h + w + B)
+    y = inputs.cast(rng.standard_normal((B, h, w)), "float32")
+    x = inputs.cast(rng.standard_normal((B, plan.p_valid)), "float32")
+    yd, xd = to_dev(torch, y, "float32"), to_dev(torch, plan.from_packed(x), "float32")
+    tol = TOL["float32"]
+    assert rel(host(plan.synthesize(xd)), O.synthesize(x, h, w, J, filt, bc)) <= tol
+    assert rel(plan.to_packed(host(plan.adjoint(yd))), O.adjoint(y, J, filt, bc)) <= tol
+    assert rel(plan.to_packed(host(plan.analyze(yd))), O.analyze(y, J, filt, bc)) <= tol
+    if blur is not None:
+        g = host(wl.grad(plan, blur, xd, yd))
+        gref, _ = O.grad(x, y, J, filt, bc)
+        assert rel(plan.to_packed(g), gref) <= tol
