@@ -5,6 +5,6 @@ for r in "$@"; do
   echo "################ $(basename $r)"
   python "$(dirname "$0")/ncu_summary.py" "$r"
   python "$(dirname "$0")/ncu_stalls.py" "$r" | grep "stalls"
-  python "$(dirname "$0")/ncu_sass_mix.py" "$r" | head -12
+  python "$(dirname "$0")/ncu_sass_mix.py" "$r" 2>/dev/null | head -12
   echo
 done
