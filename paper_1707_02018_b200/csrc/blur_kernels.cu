@@ -48,17 +48,6 @@
 namespace wl {
 namespace {
 
-// Source index of extended position p under the infinite half-point symmetric extension.
-__device__ __forceinline__ int refl_inf(int p, int n) {
-  if (p >= 0 && p < n) return p;
-  if (p < 0 && p >= -n) return -1 - p;  // single reflections (the only ones a plan with n >= h needs)
-  if (p >= n && p < 2 * n) return 2 * n - 1 - p;
-  const int m = 2 * n;
-  p %= m;
-  if (p < 0) p += m;
-  return p < n ? p : m - 1 - p;
-}
-
 template <typename T, int HW, bool RESID>
 struct BCfg {
   using P = typename Pair<T>::t;
@@ -560,11 +549,15 @@ cudaError_t dispatch_blur(const BlurArgs &a, cudaStream_t s, bool residual) {
 
 cudaError_t launch_blur(int dtype, const BlurArgs &a, cudaStream_t s) {
   if (a.batch == 0) return cudaSuccess;
+  cudaError_t e;
+  if (launch_blur_ring(dtype, a, false, s, &e)) return e;
   return dtype == WL_F64 ? dispatch_blur<double>(a, s, false) : dispatch_blur<float>(a, s, false);
 }
 
 cudaError_t launch_blur_residual(int dtype, const BlurArgs &a, cudaStream_t s) {
   if (a.batch == 0) return cudaSuccess;
+  cudaError_t e;
+  if (launch_blur_ring(dtype, a, true, s, &e)) return e;
   return dtype == WL_F64 ? dispatch_blur<double>(a, s, true) : dispatch_blur<float>(a, s, true);
 }
 

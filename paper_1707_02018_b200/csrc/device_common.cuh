@@ -37,6 +37,18 @@ __device__ __forceinline__ float4 vec_make<float>(const float *i) { return make_
 template <>
 __device__ __forceinline__ double2 vec_make<double>(const double *i) { return make_double2(i[0], i[1]); }
 
+// Source index of extended position p under the infinite half-point symmetric extension
+// (P:82 applied repeatedly): ..., y[1], y[0] | y[0], ..., y[n-1] | y[n-1], y[n-2], ...
+__device__ __forceinline__ int refl_inf(int p, int n) {
+  if (p >= 0 && p < n) return p;
+  if (p < 0 && p >= -n) return -1 - p;  // single reflections (the only ones a plan with n >= h needs)
+  if (p >= n && p < 2 * n) return 2 * n - 1 - p;
+  const int m = 2 * n;
+  p %= m;
+  if (p < 0) p += m;
+  return p < n ? p : m - 1 - p;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -136,6 +148,14 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const void *tmap, uint64_
       "[%2];\n" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
       : "memory");
+}
+
+// 1-D bulk copy global -> shared (16-byte aligned, bytes % 16 == 0); completion on `bar`.
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 
 }  // namespace wl

@@ -83,6 +83,10 @@ cudaError_t launch_synthesis(int dtype, const SynthesisArgs &a, cudaStream_t s);
 cudaError_t launch_fold(int dtype, const FoldArgs &a, cudaStream_t s);
 cudaError_t launch_blur(int dtype, const BlurArgs &a, cudaStream_t s);
 cudaError_t launch_blur_residual(int dtype, const BlurArgs &a, cudaStream_t s);
+// Register-ring kernels (blur_ring_kernels.cu): fp32, PSFs of <= 15 taps, width % 4 == 0, 16-byte
+// aligned buffers.  Returns false (nothing launched) when the arguments are outside that domain;
+// otherwise launches and stores the launch status in *err.
+bool launch_blur_ring(int dtype, const BlurArgs &a, bool residual, cudaStream_t s, cudaError_t *err);
 cudaError_t launch_zero(void *ptr, size_t bytes, cudaStream_t s);
 // FISTA pieces (fista_kernels.cu); n = elements per call (batch * p_alloc for the update)
 // Example 2: batched valid cross-correlation out_b[i] = sum_{j<ta} a_b[j] b_b[i+j]
