@@ -19,6 +19,9 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
+import shutil
+import subprocess
 import sys
 import threading
 import time
@@ -150,6 +153,76 @@ def time_calls(torch, fn, reps, warmup=3):
     return e0.elapsed_time(e1) / reps
 
 
+def time_dist(torch, fn, reps, flush=None, warmup=3):
+    """Per-call device time distribution (CUDA events on the launching stream):
+    median / p10 / p90 ms over `reps` calls.  flush: a buffer of >= 2x the L2 size zeroed before
+    every call, outside the events (cold L2); None: back-to-back calls (warm L2)."""
+    s = torch.cuda.current_stream()
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in ev:
+        if flush is not None:
+            flush.zero_()
+        a.record(s)
+        fn()
+        b.record(s)
+    torch.cuda.synchronize()
+    t = np.array([a.elapsed_time(b) for a, b in ev])
+    return {"median_ms": float(np.median(t)), "p10_ms": float(np.percentile(t, 10)),
+            "p90_ms": float(np.percentile(t, 90)), "reps": int(reps),
+            "l2": "cold (2x L2 memset before each call)" if flush is not None else "warm (back to back)"}
+
+
+def l2_flush_buffer(torch, dev):
+    """A scratch buffer of 2x the device's L2 (SURVEY §8(d) cold-L2 protocol)."""
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    return torch.empty(2 * l2 // 4 + 1024, dtype=torch.float32, device=dev), l2
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor() or "unknown"
+
+
+_ONE_THREAD = r"""
+import sys, time
+sys.path.insert(0, {root!r})
+from oracle import oracle as O
+from paper_1707_02018_b200 import inputs
+c = inputs.CONFIGS[5]
+lay = O.layout(c.h, c.w, c.levels, c.filt, c.bc)
+x, _, bl, nz = inputs.workload(c, lay.p, batch=1)
+x = inputs.cast(x, c.dtype)
+b = inputs.cast(O.blur(bl) + nz, c.dtype)
+t = time.perf_counter()
+O.grad(x, b, c.levels, c.filt, c.bc)
+print(time.perf_counter() - t)
+"""
+
+
+def cpu_oracle_one_thread(timeout=240):
+    """The fp64 oracle's cfg5 gradient on one 4096^2 image, pinned to one core with one OpenMP
+    thread (taskset + OMP_NUM_THREADS=1); seconds, or None if it cannot run."""
+    cpu = sorted(os.sched_getaffinity(0))[0]
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    cmd = [sys.executable, "-c", _ONE_THREAD.format(root=ROOT)]
+    if shutil.which("taskset"):
+        cmd = ["taskset", "-c", str(cpu)] + cmd
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=timeout)
+        return float(out.stdout.strip().splitlines()[-1])
+    except Exception:
+        return None
+
+
 # ------------------------------------------------------------------- oracle arm
 def cpu_oracle_grad_step(c, plan_p_valid, x, b):
     from oracle import oracle as O
@@ -187,7 +260,7 @@ def run_reference(args):
             "config": {"workload": "cfg5 grad f, 1 of 4 images per step (bounded sample)", "h": c.h, "w": c.w,
                        "batch": 1, "filter": c.filt, "bc": c.bc, "levels": c.levels},
             "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cores, "kind": "oracle",
-                             "sample": "1 image of 4096^2 per step (cfg5 has 4)"},
+                             "sample": "1 image of 4096^2 per step (cfg5 has 4)", "cpu_model": cpu_model()},
             "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "grad_evals_per_s": 1.0 / step_s}
     print(json.dumps(line))
@@ -243,6 +316,11 @@ def run_wl(args):
     ms_eager = ms if graph is None else max_over_ranks(time_calls(torch, step_eager, max(args.steps, 5)), ws)
     nbytes = grad_bytes(B, N, plan.p_valid, es)
     value = ws * nbytes / (ms * 1e-3) / 1e9
+    # per-step distributions beside the contract loop: cold L2 (primary) and warm
+    flush, l2_bytes = l2_flush_buffer(torch, dev)
+    dist_reps = max(args.steps, 20)
+    step_dist = {"cold": time_dist(torch, step, dist_reps, flush), "warm": time_dist(torch, step, dist_reps)}
+    step_dist["cold"]["GB/s"] = nbytes / (step_dist["cold"]["median_ms"] * 1e-3) / 1e9
 
     # ---- per-kernel live timing (events on the launching stream) for the roofline object
     u = torch.empty(B, c.h, c.w, device=dev)
@@ -259,6 +337,13 @@ def run_wl(args):
     kernels["analysis_level1_Wstar"] = {"ms": t_a1, "bytes": es * B * (N + p1.p_valid)}
     t_s1 = time_calls(torch, lambda: p1.synthesize(x1, out=u), reps)
     kernels["synthesis_level1_W"] = {"ms": t_s1, "bytes": es * B * (N + p1.p_valid)}
+    # the same kernels with the cold-L2 protocol (median, p10 / p90)
+    cold = {"blur_residual_adjoint": time_dist(torch, lambda: blur.residual_adjoint(u, b, out=sres), reps, flush),
+            "analysis_level1_Wstar": time_dist(torch, lambda: p1.adjoint(u, out=x1), reps, flush),
+            "synthesis_level1_W": time_dist(torch, lambda: p1.synthesize(x1, out=u), reps, flush)}
+    for name, d in cold.items():
+        kernels[name]["cold"] = d
+        kernels[name]["cold"]["GB/s"] = kernels[name]["bytes"] / (d["median_ms"] * 1e-3) / 1e9
     for k in kernels.values():
         k["GB/s"] = k["bytes"] / (k["ms"] * 1e-3) / 1e9
         k["frac"] = k["GB/s"] / hbm_peak
@@ -279,10 +364,17 @@ def run_wl(args):
     y4 = torch.from_numpy(y4.astype(np.float32)).to(dev)
     x4 = torch.empty(1, plan4.p_alloc, device=dev)
     ws4 = plan4._ws(wl.OP_ADJOINT, 1)
-    t4 = time_calls(torch, wl.Graph(lambda: plan4.adjoint(y4, out=x4, ws=ws4)).replay, max(args.steps, 20))
+    g4 = wl.Graph(lambda: plan4.adjoint(y4, out=x4, ws=ws4))
     b4 = 4 * (c4.h * c4.w + plan4.p_valid)
+    d4c = time_dist(torch, g4.replay, max(args.steps, 30), flush)       # primary: cold L2
+    d4w = time_dist(torch, g4.replay, max(args.steps, 30))              # beside it: warm
+    t4 = d4c["median_ms"]
+    t4e = time_dist(torch, lambda: plan4.adjoint(y4, out=x4, ws=ws4), max(args.steps, 30), flush)
     wstar = {"us": t4 * 1e3, "GB/s": b4 / (t4 * 1e-3) / 1e9, "frac": b4 / (t4 * 1e-3) / 1e9 / hbm_peak,
-             "bytes": b4, "config": "cfg4 4096^2 db8 zero 6 levels fp32", "launch": "cuda_graph"}
+             "bytes": b4, "config": "cfg4 4096^2 db8 zero 6 levels fp32", "launch": "cuda_graph",
+             "l2": "cold (2x L2 memset before each call); warm beside it", "cold": d4c, "warm": d4w,
+             "warm_us": d4w["median_ms"] * 1e3, "eager_cold_us": t4e["median_ms"] * 1e3,
+             "traffic": traffic_from_profiles("wstar_cfg4_chain")}
     del y4, x4, ws4
 
     # ---- one FISTA iteration at cfg5 (grad f(y) + fused prox/momentum update)
@@ -363,11 +455,17 @@ def run_wl(args):
         x1h, _, bl1, nz1 = inputs.workload(c, plan.p_valid, batch=1)
         x1h = inputs.cast(x1h, c.dtype)
         b1 = inputs.cast(O.blur(bl1) + nz1, c.dtype)
-        reps_cpu = 2
-        t = min(cpu_oracle_grad_step(c, plan.p_valid, x1h, b1) for _ in range(reps_cpu))
-        cpu = {"value": grad_bytes(1, N, plan.p_valid, es) / t / 1e9, "unit": "GB/s",
-               "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
-               "sample": f"1 of the 4 cfg5 images (4096^2), best of {reps_cpu}", "s_per_image": t}
+        reps_cpu = 3
+        ts = sorted(cpu_oracle_grad_step(c, plan.p_valid, x1h, b1) for _ in range(reps_cpu))
+        t = ts[len(ts) // 2]
+        nb1 = grad_bytes(1, N, plan.p_valid, es)
+        t1 = None if args.no_single_thread else cpu_oracle_one_thread()
+        cpu = {"value": nb1 / t / 1e9, "unit": "GB/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+               "sample": f"1 of the 4 cfg5 images (4096^2) per timing, median of {reps_cpu}, all host cores (OpenMP)",
+               "s_per_image": t, "cpu_model": cpu_model(),
+               "single_thread": None if t1 is None else {
+                   "value": nb1 / t1 / 1e9, "unit": "GB/s", "cores": 1, "s_per_image": t1,
+                   "sample": "1 cfg5 image, taskset to one core, OMP_NUM_THREADS=1, one timing"}}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
@@ -382,7 +480,7 @@ def run_wl(args):
                            "bytes_per_step_per_gpu": nbytes},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(), "step_launch": "eager" if graph is None else "cuda_graph",
-                "ms_per_step_eager": ms_eager, "grad_evals_per_s": ws / (ms * 1e-3), "images_per_s": ws * B / (ms * 1e-3),
+                "ms_per_step_eager": ms_eager, "step_distribution": step_dist, "l2_bytes": l2_bytes, "grad_evals_per_s": ws / (ms * 1e-3), "images_per_s": ws * B / (ms * 1e-3),
                 "grad_frac_of_hbm_roofline": value / ws / hbm_peak, "wstar_cfg4": wstar, "fista_cfg5": fista, "bce": bce, "operators_by_config": per_cfg, "kernels": kernels}
         print(json.dumps(line))
     if ws > 1:
@@ -398,6 +496,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="wl", choices=["wl", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-single-thread", action="store_true", help="skip the one-core oracle timing")
     ap.add_argument("--eager", action="store_true", help="launch the timed step eagerly instead of as a CUDA graph")
     args = ap.parse_args()
     if args.impl == "reference":

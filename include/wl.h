@@ -228,17 +228,20 @@ WL_API wl_status wl_grad_adj(const wl_plan *plan, const wl_blur_plan *blur, int6
  * wl_fista_update: given g = grad f(y) [batch, p_alloc], in place
  *     x <- soft(y - g / lip, lambda / lip),  t+ = (1 + sqrt(1 + 4 t^2)) / 2,
  *     y <- x + ((t - 1) / t+) (x - x_old).
- * t is the host-side momentum scalar of the current step (t_1 = 1; the caller advances it with
- * the same formula).  lip > 0 is the Lipschitz constant of grad f (wl_lipschitz), lambda >= 0.
- * Pitch padding stays 0.  x, y, g must not overlap (WL_EINVAL). */
+ * t is the host-side momentum scalar of the current step (t_1 = 1); *t_next_host (host pointer,
+ * nullable) receives t+ for the next call, so the recursion lives in the library only.  lip > 0 is
+ * the Lipschitz constant of grad f (wl_lipschitz), lambda >= 0.  Pitch padding stays 0.  x, y, g
+ * must not overlap (WL_EINVAL). */
 WL_API wl_status wl_fista_update(const wl_plan *plan, int64_t batch, const void *g, void *x, void *y, double t,
-                          double lambda, double lip, void *stream);
+                          double lambda, double lip, double *t_next_host, void *stream);
 /* One full FISTA iteration: g = grad f(y) (wl_grad_adj with `adj`; f_dev, nullable, receives
  * f(y)), then the wl_fista_update arithmetic, fused into the stores of the closing analysis
- * chain: g itself is never written.  ws: wl_workspace_bytes(plan, blur, WL_OP_FISTA, batch). */
+ * chain: g itself is never written.  *t_next_host (nullable) receives t_{k+1}, written before the
+ * call returns (the launches stay asynchronous).  ws: wl_workspace_bytes(plan, blur, WL_OP_FISTA,
+ * batch). */
 WL_API wl_status wl_fista_step(const wl_plan *plan, const wl_blur_plan *blur, int64_t batch, const void *b, void *x,
                         void *y, double t, double lambda, double lip, double *f_dev, wl_adj adj, void *ws,
-                        void *stream);
+                        double *t_next_host, void *stream);
 /* wl_fista_step with the momentum scalar t resident on the device: t_dev (double, device) holds
  * t_k on entry and t_{k+1} on exit (advanced by a one-thread kernel after the update).  Every
  * argument of the launch sequence is then the same from one iteration to the next, so a CUDA

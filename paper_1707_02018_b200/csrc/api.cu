@@ -50,6 +50,10 @@ wl_status cuda_fail(cudaError_t e, const char *what) {
 }
 
 int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+// FISTA momentum recursion t_{k+1} = (1 + sqrt(1 + 4 t_k^2)) / 2 (Beck & Teboulle, cited at P:117;
+// DESIGN.md reading R21); the device-resident variant is k_fista_advance_t.
+double fista_next_t(double t) { return (1.0 + std::sqrt(1.0 + 4.0 * t * t)) / 2.0; }
 size_t align256(size_t v) { return (v + 255) / 256 * 256; }
 
 const char *bc_name(int bc) {
@@ -79,6 +83,8 @@ wl_status check_dev(const void *p, const char *name, size_t align = 16) {
 }
 
 constexpr size_t kMaxSmemOptin = 227 * 1024;  // sm_100a opt-in dynamic shared memory per CTA
+// the launch structures carry the batch as int (grid dimensions and per-image offsets)
+constexpr int kMaxBatch = 0x7fffffff;
 
 bool overlap(const void *a, size_t na, const void *b, size_t nb) {
   auto x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
@@ -440,6 +446,7 @@ static wl_status analysis_entry(const wl_plan *p, int64_t batch, const void *img
                                 bool adjoint, const char *name) {
   if (check_plan(p)) return WL_EINVAL;
   if (batch < 0) return fail(WL_EINVAL, "%s: batch=%lld < 0", name, (long long)batch);
+  if (batch > kMaxBatch) return fail(WL_ESIZE, "%s: batch=%lld exceeds %d", name, (long long)batch, kMaxBatch);
   if (batch == 0) return ok();
   size_t ib = (size_t)batch * p->h * p->w * p->es, xb = (size_t)batch * p->p_alloc * p->es;
   wl_status st = check_io(img, ib, "img", x, xb, "x");
@@ -463,6 +470,7 @@ wl_status wl_analyze(const wl_plan *p, int64_t batch, const void *img, void *x, 
 wl_status wl_synthesize(const wl_plan *p, int64_t batch, const void *x, void *img, void *ws, void *stream) {
   if (check_plan(p)) return WL_EINVAL;
   if (batch < 0) return fail(WL_EINVAL, "wl_synthesize: batch=%lld < 0", (long long)batch);
+  if (batch > kMaxBatch) return fail(WL_ESIZE, "wl_synthesize: batch=%lld exceeds %d", (long long)batch, kMaxBatch);
   if (batch == 0) return ok();
   size_t ib = (size_t)batch * p->h * p->w * p->es, xb = (size_t)batch * p->p_alloc * p->es;
   wl_status st = check_io(x, xb, "x", img, ib, "img");
@@ -478,6 +486,7 @@ wl_status wl_synthesize(const wl_plan *p, int64_t batch, const void *x, void *im
 wl_status wl_analyze_adjoint(const wl_plan *p, int64_t batch, const void *x, void *img, void *ws, void *stream) {
   if (check_plan(p)) return WL_EINVAL;
   if (batch < 0) return fail(WL_EINVAL, "wl_analyze_adjoint: batch=%lld < 0", (long long)batch);
+  if (batch > kMaxBatch) return fail(WL_ESIZE, "wl_analyze_adjoint: batch=%lld exceeds %d", (long long)batch, kMaxBatch);
   if (batch == 0) return ok();
   size_t ib = (size_t)batch * p->h * p->w * p->es, xb = (size_t)batch * p->p_alloc * p->es;
   wl_status st = check_io(x, xb, "x", img, ib, "img");
@@ -544,6 +553,7 @@ static wl_status blur_entry(const wl_blur_plan *bl, int64_t batch, const void *i
                             const char *name) {
   if (!bl) return fail(WL_EINVAL, "%s: blur plan is NULL", name);
   if (batch < 0) return fail(WL_EINVAL, "%s: batch=%lld < 0", name, (long long)batch);
+  if (batch > kMaxBatch) return fail(WL_ESIZE, "%s: batch=%lld exceeds %d", name, (long long)batch, kMaxBatch);
   if (batch == 0) return ok();
   size_t ib = (size_t)batch * bl->h * bl->w * bl->es;
   wl_status st = check_io(in, ib, "in", out, ib, "out");
@@ -593,6 +603,7 @@ wl_status wl_blur_residual_adjoint(const wl_blur_plan *bl, int64_t batch, const 
                                    double *f_dev, void *stream) {
   if (!bl) return fail(WL_EINVAL, "blur plan is NULL");
   if (batch < 0) return fail(WL_EINVAL, "batch=%lld < 0", (long long)batch);
+  if (batch > kMaxBatch) return fail(WL_ESIZE, "batch=%lld exceeds %d", (long long)batch, kMaxBatch);
   if (batch == 0) return ok();
   size_t ib = (size_t)batch * bl->h * bl->w * bl->es;
   wl_status st = check_io(u, ib, "u", s, ib, "s");
@@ -619,6 +630,7 @@ wl_status wl_grad_adj(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, c
                 (long long)bl->w, (long long)p->h, (long long)p->w);
   if (bl->dtype != p->dtype) return fail(WL_EDTYPE, "wl_grad: blur and wavelet plans have different dtypes");
   if (batch < 0) return fail(WL_EINVAL, "wl_grad: batch=%lld < 0", (long long)batch);
+  if (batch > kMaxBatch) return fail(WL_ESIZE, "wl_grad: batch=%lld exceeds %d", (long long)batch, kMaxBatch);
   if (batch == 0) return ok();
   size_t ib = (size_t)batch * p->h * p->w * p->es, xb = (size_t)batch * p->p_alloc * p->es;
   wl_status st = check_io(x, xb, "x", g, xb, "g");
@@ -641,19 +653,42 @@ wl_status wl_grad_host(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, 
   if (bl->h != p->h || bl->w != p->w || bl->dtype != p->dtype)
     return fail(WL_EINVAL, "wl_grad_host: blur plan does not match the wavelet plan");
   if (batch < 0) return fail(WL_EINVAL, "wl_grad_host: batch=%lld < 0", (long long)batch);
+  if (batch > kMaxBatch) return fail(WL_ESIZE, "wl_grad_host: batch=%lld exceeds %d", (long long)batch, kMaxBatch);
   if (batch == 0) return ok();
   if (!x_host || !b_host || !g_host) return fail(WL_EINVAL, "wl_grad_host: x_host, b_host and g_host must be non-NULL");
   wl_status st;
   if ((st = check_ws(p, bl, WL_OP_GRAD_HOST, batch, ws))) return st;
   const WsLayout L = ws_layout(p, bl, WL_OP_GRAD_HOST, batch);
   const size_t es = (size_t)p->es, xs = (size_t)p->p_alloc * es, is = (size_t)p->h * p->w * es;
-  cudaStream_t s = (cudaStream_t)stream, cin = nullptr, cout = nullptr;
-  cudaEvent_t ev[7] = {};  // start, in[2], done[2], free[2]
-  cudaError_t e = cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking);
-  for (int i = 0; i < 7 && e == cudaSuccess; i++) e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+  cudaStream_t s = (cudaStream_t)stream;
+  // copy streams and events: created once per (thread, device) and reused by every call
+  struct HostPipe {
+    int dev = -1;
+    cudaStream_t cin = nullptr, cout = nullptr;
+    cudaEvent_t ev[7] = {};  // start, in[2], done[2], free[2]
+  };
+  thread_local HostPipe pipes[8];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "wl_grad_host device");
+  HostPipe *hp = nullptr;
+  for (auto &q : pipes)
+    if (q.dev == dev || q.dev < 0) {
+      hp = &q;
+      break;
+    }
+  if (!hp) return fail(WL_EINVAL, "wl_grad_host: more than 8 devices used from one thread");
+  if (hp->dev < 0) {
+    e = cudaStreamCreateWithFlags(&hp->cin, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&hp->cout, cudaStreamNonBlocking);
+    for (int i = 0; i < 7 && e == cudaSuccess; i++) e = cudaEventCreateWithFlags(&hp->ev[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(e, "wl_grad_host stream setup");
+    hp->dev = dev;
+  }
+  cudaStream_t cin = hp->cin, cout = hp->cout;
+  cudaEvent_t *ev = hp->ev;
   char *w = (char *)ws;
-  if (e == cudaSuccess) e = cudaEventRecord(ev[0], s);  // the call is ordered after prior work on `stream`
+  e = cudaEventRecord(ev[0], s);  // the call is ordered after prior work on `stream`
   if (e == cudaSuccess) e = cudaStreamWaitEvent(cin, ev[0], 0);
   for (int64_t i = 0; i < batch && e == cudaSuccess && !st; i++) {
     const int k = (int)(i & 1);
@@ -673,25 +708,31 @@ wl_status wl_grad_host(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, 
     if (e == cudaSuccess && f_host) e = cudaMemcpyAsync(f_host + i, df, sizeof(double), cudaMemcpyDeviceToHost, cout);
     if (e == cudaSuccess) e = cudaEventRecord(ev[5 + k], cout);
   }
-  // `stream` resumes after the last copy out
-  if (e == cudaSuccess && !st) e = cudaEventRecord(ev[0], cout);
-  if (e == cudaSuccess && !st) e = cudaStreamWaitEvent(s, ev[0], 0);
-  for (int i = 0; i < 7; i++)
-    if (ev[i]) cudaEventDestroy(ev[i]);  // released once their pending work completes
-  if (cin) cudaStreamDestroy(cin);
-  if (cout) cudaStreamDestroy(cout);
+  // `stream` resumes after every copy this call queued, on success and on failure alike, so the
+  // caller never reuses ws or the host buffers while a copy is in flight
+  cudaError_t e2 = cudaEventRecord(ev[0], cout);
+  if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(s, ev[0], 0);
+  if (e2 == cudaSuccess) e2 = cudaEventRecord(ev[0], cin);
+  if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(s, ev[0], 0);
+  if (e2 != cudaSuccess) {
+    cudaStreamSynchronize(cin);
+    cudaStreamSynchronize(cout);
+  }
   if (st) return st;
   if (e != cudaSuccess) return cuda_fail(e, "wl_grad_host pipeline");
+  if (e2 != cudaSuccess) return cuda_fail(e2, "wl_grad_host pipeline");
   return ok();
 }
 
 wl_status wl_fista_update(const wl_plan *p, int64_t batch, const void *g, void *x, void *y, double t, double lambda,
-                          double lip, void *stream) {
+                          double lip, double *t_next_host, void *stream) {
   if (check_plan(p)) return WL_EINVAL;
   if (batch < 0) return fail(WL_EINVAL, "wl_fista_update: batch=%lld < 0", (long long)batch);
+  if (batch > kMaxBatch) return fail(WL_ESIZE, "wl_fista_update: batch=%lld exceeds %d", (long long)batch, kMaxBatch);
   if (!(lip > 0) || !std::isfinite(lip)) return fail(WL_EINVAL, "wl_fista_update: lip=%g must be > 0", lip);
   if (!(lambda >= 0) || !std::isfinite(lambda)) return fail(WL_EINVAL, "wl_fista_update: lambda=%g must be >= 0", lambda);
   if (!(t >= 1) || !std::isfinite(t)) return fail(WL_EINVAL, "wl_fista_update: t=%g must be >= 1", t);
+  if (t_next_host) *t_next_host = fista_next_t(t);
   if (batch == 0) return ok();
   const size_t xb = (size_t)batch * p->p_alloc * p->es;
   wl_status st;
@@ -706,15 +747,17 @@ wl_status wl_fista_update(const wl_plan *p, int64_t batch, const void *g, void *
 
 static wl_status fista_step_core(const char *fn, const wl_plan *p, const wl_blur_plan *bl, int64_t batch,
                                  const void *b, void *x, void *y, double t, double *t_dev, double lambda, double lip,
-                                 double *f_dev, wl_adj adj, void *ws, void *stream) {
+                                 double *f_dev, wl_adj adj, void *ws, double *t_next_host, void *stream) {
   if (check_plan(p)) return WL_EINVAL;
   if (adj != WL_ADJ_TRUE && adj != WL_ADJ_PINV) return fail(WL_EINVAL, "%s: adj=%d is not a wl_adj", fn, (int)adj);
   if (!bl) return fail(WL_EINVAL, "%s: blur plan is NULL", fn);
   if (bl->h != p->h || bl->w != p->w || bl->dtype != p->dtype)
     return fail(WL_EINVAL, "%s: blur plan does not match the wavelet plan", fn);
   if (batch < 0) return fail(WL_EINVAL, "%s: batch=%lld < 0", fn, (long long)batch);
+  if (batch > kMaxBatch) return fail(WL_ESIZE, "%s: batch=%lld exceeds %d", fn, (long long)batch, kMaxBatch);
   if (!(lip > 0) || !(lambda >= 0) || !(t_dev || t >= 1))
     return fail(WL_EINVAL, "%s: need lip > 0, lambda >= 0, t >= 1", fn);
+  if (!t_dev && t_next_host) *t_next_host = fista_next_t(t);
   if (batch == 0) return ok();
   const size_t ib = (size_t)batch * p->h * p->w * p->es, xb = (size_t)batch * p->p_alloc * p->es;
   wl_status st;
@@ -733,7 +776,7 @@ static wl_status fista_step_core(const char *fn, const wl_plan *p, const wl_blur
   // (g never reaches HBM).  W reads y before the W* chain rewrites it (stream order).
   if ((st = run_synthesis(p, batch, y, w + L.u, w, L, s))) return st;
   if ((st = residual_core(bl, batch, w + L.u, b, w + L.s, f_dev, s))) return st;
-  const double t_new = (1.0 + std::sqrt(1.0 + 4.0 * t * t)) / 2.0;
+  const double t_new = fista_next_t(t);
   const FistaFuse fz{x, 1.0 / lip, lambda / lip, t_dev ? 0.0 : (t - 1.0) / t_new, t_dev};
   if ((st = run_analysis(p, batch, w + L.s, y, w, L, adj == WL_ADJ_TRUE, s, &fz))) return st;
   if (t_dev) {
@@ -744,15 +787,17 @@ static wl_status fista_step_core(const char *fn, const wl_plan *p, const wl_blur
 }
 
 wl_status wl_fista_step(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, const void *b, void *x, void *y,
-                        double t, double lambda, double lip, double *f_dev, wl_adj adj, void *ws, void *stream) {
-  return fista_step_core("wl_fista_step", p, bl, batch, b, x, y, t, nullptr, lambda, lip, f_dev, adj, ws, stream);
+                        double t, double lambda, double lip, double *f_dev, wl_adj adj, void *ws, double *t_next_host,
+                        void *stream) {
+  return fista_step_core("wl_fista_step", p, bl, batch, b, x, y, t, nullptr, lambda, lip, f_dev, adj, ws, t_next_host,
+                         stream);
 }
 
 wl_status wl_fista_step_dev(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, const void *b, void *x, void *y,
                             double *t_dev, double lambda, double lip, double *f_dev, wl_adj adj, void *ws,
                             void *stream) {
   if (!t_dev) return fail(WL_EINVAL, "wl_fista_step_dev: t_dev is NULL");
-  return fista_step_core("wl_fista_step_dev", p, bl, batch, b, x, y, 1.0, t_dev, lambda, lip, f_dev, adj, ws,
+  return fista_step_core("wl_fista_step_dev", p, bl, batch, b, x, y, 1.0, t_dev, lambda, lip, f_dev, adj, ws, nullptr,
                          stream);
 }
 
@@ -805,6 +850,7 @@ wl_status wl_lipschitz(const wl_plan *p, const wl_blur_plan *bl, int iters, uint
 static wl_status bce_sizes(const char *fn, wl_dtype dtype, int64_t batch, int64_t K, int64_t N) {
   if (dtype != WL_F32 && dtype != WL_F64) return fail(WL_EDTYPE, "%s: dtype=%d", fn, (int)dtype);
   if (batch < 0) return fail(WL_EINVAL, "%s: batch=%lld < 0", fn, (long long)batch);
+  if (batch > kMaxBatch) return fail(WL_ESIZE, "%s: batch=%lld exceeds %d", fn, (long long)batch, kMaxBatch);
   if (K < 1 || N < 1) return fail(WL_ESIZE, "%s: K=%lld and N=%lld must be >= 1", fn, (long long)K, (long long)N);
   if (K + N > (int64_t)1 << 24) return fail(WL_ESIZE, "%s: K+N=%lld too long", fn, (long long)(K + N));
   return WL_OK;

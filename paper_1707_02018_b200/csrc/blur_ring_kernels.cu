@@ -296,17 +296,24 @@ __global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_co
         // output row of step 0 of this group (stage 1 for R, stage 2 for the residual)
         float *orow = obase + (long long)((RESID ? brow0 : urow0) + k * G - HW) * w;
         // ---------------- stage 1: h1 = R_h u -> ring1; r = R_v h1 - b (residual) or out = R_v h1
+        // (the window of step r + 1 is loaded before step r computes: WL_RING_PF)
+        float2 wb[2][NWIN / 2];
+#pragma unroll
+        for (int j = 0; j < NWIN / 2; j++) wb[0][j] = reinterpret_cast<const float2 *>(ub)[j];
 #pragma unroll
         for (int r = 0; r < G; r++) {
           const int slot = gg * G + r;  // == step % kRing (kb G is a multiple of kRing)
           const int i = k * G + r;
+          if (r + 1 < G) {
+            const float2 *src = reinterpret_cast<const float2 *>(ub + (r + 1) * C::UBOX);
+#pragma unroll
+            for (int j = 0; j < NWIN / 2; j++) wb[(r + 1) & 1][j] = src[j];
+          }
           float win[NWIN];
-          const float2 *src = reinterpret_cast<const float2 *>(ub + r * C::UBOX);
 #pragma unroll
           for (int j = 0; j < NWIN / 2; j++) {
-            const float2 v = src[j];
-            win[2 * j] = v.x;
-            win[2 * j + 1] = v.y;
+            win[2 * j] = wb[r & 1][j].x;
+            win[2 * j + 1] = wb[r & 1][j].y;
           }
           ring1[slot] = hpair<HW, S0>(win, p);
           if (RESID) {
@@ -330,17 +337,23 @@ __global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_co
             __syncthreads();
           }
           // ---------------- stage 2: h2 = R_h r -> ring2; s = R_v h2
+          const float2 *rsrc = reinterpret_cast<const float2 *>(rw + 2 * tid);
+          float2 vb[2][NWIN / 2];
+#pragma unroll
+          for (int j = 0; j < NWIN / 2; j++) vb[0][j] = rsrc[j];
 #pragma unroll
           for (int r = 0; r < G; r++) {
             const int slot = gg * G + r;
             const int i = k * G + r;
+            if (r + 1 < G) {
+#pragma unroll
+              for (int j = 0; j < NWIN / 2; j++) vb[(r + 1) & 1][j] = rsrc[(r + 1) * (C::NC / 2) + j];
+            }
             float win[NWIN];
-            const float2 *src = reinterpret_cast<const float2 *>(rw + r * C::NC + 2 * tid);
 #pragma unroll
             for (int j = 0; j < NWIN / 2; j++) {
-              const float2 v = src[j];
-              win[2 * j] = v.x;
-              win[2 * j + 1] = v.y;
+              win[2 * j] = vb[r & 1][j].x;
+              win[2 * j + 1] = vb[r & 1][j].y;
             }
             ring2[slot] = hpair<HW, 0>(win, p);
             const float2 o = vring<HW>(ring2, slot, p, make_float2(0.f, 0.f));

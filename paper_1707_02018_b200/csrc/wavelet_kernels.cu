@@ -21,11 +21,12 @@ namespace {
 template <typename T>
 __global__ void __launch_bounds__(256) k_fold_sym_pinv(const T *__restrict__ U, long long upitch, long long ubs,
                                                        T *__restrict__ y, long long ypitch, long long ybs, int n0,
-                                                       int n1, int Lp, int weighted, int vec) {
+                                                       int n1, int Lp, int weighted, int vec, long long nrows) {
   const int p0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
-  const int i = blockIdx.y;
-  const int b = blockIdx.z;
   if (p0 >= n1) return;
+  // (image, row) pairs flattened over gridDim.y with a stride loop: any batch and height
+  for (long long ib = blockIdx.y; ib < nrows; ib += gridDim.y) {
+  const int b = (int)(ib / n0), i = (int)(ib - (long long)b * n0);
   const T *u = U + (long long)b * ubs;
   T *yo = y + (long long)b * ybs + (long long)i * ypitch;
   const bool row_in = i >= Lp && i < n0 - Lp;
@@ -41,7 +42,7 @@ __global__ void __launch_bounds__(256) k_fold_sym_pinv(const T *__restrict__ U, 
 #pragma unroll
       for (int k = 0; k < 4; k++) yo[p0 + k] = v[k];
     }
-    return;
+    continue;
   }
   int t0s[3], c0 = 0;
   t0s[c0++] = i;
@@ -59,6 +60,7 @@ __global__ void __launch_bounds__(256) k_fold_sym_pinv(const T *__restrict__ U, 
       for (int c = 0; c < c1; c++) acc += u[(long long)(t0s[a] + Lp) * upitch + (t1s[c] + Lp)];
     yo[pcol] = weighted ? acc / T(c0 * c1) : acc;
   }
+  }
 }
 
 }  // namespace
@@ -66,15 +68,16 @@ __global__ void __launch_bounds__(256) k_fold_sym_pinv(const T *__restrict__ U, 
 cudaError_t launch_fold(int dtype, const FoldArgs &a, cudaStream_t s) {
   if (a.batch == 0) return cudaSuccess;
   const int vec = (a.out_pitch % 4 == 0) && (a.out_bstride % 4 == 0) && (reinterpret_cast<uintptr_t>(a.out) % 16 == 0);
-  dim3 grid((a.n1 + 4 * 256 - 1) / (4 * 256), a.n0, a.batch);
+  const long long nrows = (long long)a.n0 * a.batch;
+  dim3 grid((a.n1 + 4 * 256 - 1) / (4 * 256), (unsigned)std::min<long long>(nrows, 65535));
   if (dtype == WL_F64)
     k_fold_sym_pinv<double><<<grid, 256, 0, s>>>(static_cast<const double *>(a.in), a.in_pitch, a.in_bstride,
                                                  static_cast<double *>(a.out), a.out_pitch, a.out_bstride, a.n0,
-                                                 a.n1, a.Lp, a.weighted, vec);
+                                                 a.n1, a.Lp, a.weighted, vec, nrows);
   else
     k_fold_sym_pinv<float><<<grid, 256, 0, s>>>(static_cast<const float *>(a.in), a.in_pitch, a.in_bstride,
                                                static_cast<float *>(a.out), a.out_pitch, a.out_bstride, a.n0,
-                                               a.n1, a.Lp, a.weighted, vec);
+                                               a.n1, a.Lp, a.weighted, vec, nrows);
   g_launches++;
   return cudaGetLastError();
 }

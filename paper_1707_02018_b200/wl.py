@@ -86,10 +86,10 @@ def lib():
     L.wl_blur_adjoint.argtypes = [vp, i64, vp, vp, vp]
     L.wl_blur_residual_adjoint.argtypes = [vp, i64, vp, vp, vp, vp, vp]
     L.wl_grad.argtypes = [vp, vp, i64, vp, vp, vp, vp, vp, vp]
-    L.wl_fista_update.argtypes = [vp, i64, vp, vp, vp, cd, cd, cd, vp]
+    L.wl_fista_update.argtypes = [vp, i64, vp, vp, vp, cd, cd, cd, dp, vp]
     L.wl_grad_host.argtypes = [vp, vp, i64, vp, vp, vp, vp, vp, vp]
     L.wl_grad_adj.argtypes = [vp, vp, i64, vp, vp, vp, vp, ci, vp, vp]
-    L.wl_fista_step.argtypes = [vp, vp, i64, vp, vp, vp, cd, cd, cd, vp, ci, vp, vp]
+    L.wl_fista_step.argtypes = [vp, vp, i64, vp, vp, vp, cd, cd, cd, vp, ci, vp, dp, vp]
     L.wl_fista_step_dev.argtypes = [vp, vp, i64, vp, vp, vp, vp, cd, cd, vp, ci, vp, vp]
     L.wl_lipschitz.argtypes = [vp, vp, ci, ctypes.c_uint64, dp, vp, vp]
     for fn in ("wl_conv_full", "wl_conv_adjoint_h", "wl_conv_adjoint_s"):
@@ -149,6 +149,39 @@ def _require(t, name, dtype, shape=None):
         raise ValueError(f"{name} has shape {tuple(t.shape)}, expected [..., {', '.join(map(str, shape))}]")
 
 
+def _lead(t, trailing):
+    """Product of the leading (batch) dims of a [..., trailing dims] tensor."""
+    return int(np.prod(t.shape[:-trailing])) if t.dim() > trailing else 1
+
+
+def _same_batch(B, *items):
+    """Every (tensor, name, trailing) item must carry the batch B (the C side reads batch * size)."""
+    for t, name, trailing in items:
+        if t is not None and _lead(t, trailing) != B:
+            raise ValueError(f"{name} has batch {_lead(t, trailing)} (shape {tuple(t.shape)}), expected {B}")
+
+
+def _check_f(f, B):
+    """f: optional float64 CUDA tensor of exactly B elements (one objective value per image)."""
+    if f is not None:
+        _require(f, "f", _torch().float64)
+        if f.numel() != B:
+            raise ValueError(f"f has {f.numel()} elements, expected one per image ({B})")
+
+
+def _adopt(stream, *tensors):
+    """Tensors allocated here on the current stream but used by kernels on `stream`: tell the
+    caching allocator (record_stream) so their blocks are not reused while those kernels run."""
+    if stream is None:
+        return
+    torch = _torch()
+    if stream == torch.cuda.current_stream():
+        return
+    for t in tensors:
+        if t is not None:
+            t.record_stream(stream)
+
+
 @dataclass(frozen=True)
 class Band:
     name: str
@@ -202,7 +235,7 @@ class Plan:
     def workspace_bytes(self, op, batch, blur=None):
         return int(lib().wl_workspace_bytes(self._h, blur._h if blur is not None else None, op, int(batch)))
 
-    def _ws(self, op, batch, blur=None, ws=None):
+    def _ws(self, op, batch, blur=None, ws=None, stream=None):
         n = self.workspace_bytes(op, batch, blur)
         if ws is not None:
             if ws.numel() * ws.element_size() < n:
@@ -211,7 +244,9 @@ class Plan:
         if n == 0:
             return None
         torch = _torch()
-        return torch.empty(n, dtype=torch.uint8, device="cuda")
+        w = torch.empty(n, dtype=torch.uint8, device="cuda")
+        _adopt(stream, w)   # the kernels on `stream` own it until they finish
+        return w
 
     def _batch_of(self, t, trailing):
         return int(np.prod(t.shape[:-trailing])) if t.dim() > trailing else 1
@@ -222,8 +257,10 @@ class Plan:
         B = self._batch_of(x, 1)
         if out is None:
             out = torch.empty(x.shape[:-1] + (self.h, self.w), dtype=x.dtype, device=x.device)
+            _adopt(stream, out)
         _require(out, "img", self.torch_dtype, (self.h, self.w))
-        ws = self._ws(op, B, ws=ws)
+        _same_batch(B, (out, "img", 2))
+        ws = self._ws(op, B, ws=ws, stream=stream)
         _check(fn(self._h, B, _ptr(x), _ptr(out), _ptr(ws), _stream_ptr(stream)))
         return out
 
@@ -241,8 +278,10 @@ class Plan:
         B = self._batch_of(img, 2)
         if out is None:
             out = torch.empty(img.shape[:-2] + (self.p_alloc,), dtype=img.dtype, device=img.device)
+            _adopt(stream, out)
         _require(out, "x", self.torch_dtype, (self.p_alloc,))
-        ws = self._ws(op, B, ws=ws)
+        _same_batch(B, (out, "x", 1))
+        ws = self._ws(op, B, ws=ws, stream=stream)
         _check(fn(self._h, B, _ptr(img), _ptr(out), _ptr(ws), _stream_ptr(stream)))
         return out
 
@@ -323,7 +362,9 @@ class Blur:
         B = int(np.prod(img.shape[:-2])) if img.dim() > 2 else 1
         if out is None:
             out = torch.empty_like(img)
+            _adopt(stream, out)
         _require(out, "out", self.torch_dtype, (self.h, self.w))
+        _same_batch(B, (out, "out", 2))
         _check(fn(self._h, B, _ptr(img), _ptr(out), _stream_ptr(stream)))
         return out
 
@@ -343,8 +384,10 @@ class Blur:
         B = int(np.prod(u.shape[:-2])) if u.dim() > 2 else 1
         if out is None:
             out = torch.empty_like(u)
-        if f is not None:
-            _require(f, "f", torch.float64)
+            _adopt(stream, out)
+        _require(out, "out", self.torch_dtype, (self.h, self.w))
+        _same_batch(B, (b, "b", 2), (out, "out", 2))
+        _check_f(f, B)
         _check(lib().wl_blur_residual_adjoint(self._h, B, _ptr(u), _ptr(b), _ptr(out), _ptr(f),
                                               _stream_ptr(stream)))
         return out
@@ -376,7 +419,7 @@ def grad_host(plan: Plan, blur: Blur, x, b, out=None, f=None, ws=None, stream=No
         out = torch.empty(x.shape, dtype=x.dtype, pin_memory=x.is_pinned())
     if out.is_cuda or not out.is_contiguous() or out.shape != x.shape or out.dtype != x.dtype:
         raise ValueError("out must be a contiguous CPU tensor shaped like x")
-    if f is not None and (f.is_cuda or f.dtype != torch.float64 or f.numel() != B):
+    if f is not None and (f.is_cuda or f.dtype != torch.float64 or f.numel() != B or not f.is_contiguous()):
         raise ValueError("f must be a CPU float64 tensor of batch elements")
     ws = plan._ws(OP_GRAD_HOST, B, blur=blur, ws=ws)
     st = _stream_ptr(stream)
@@ -399,9 +442,11 @@ def grad(plan: Plan, blur: Blur, x, b, out=None, f=None, ws=None, stream=None, a
     B = int(np.prod(x.shape[:-1])) if x.dim() > 1 else 1
     if out is None:
         out = torch.empty_like(x)
-    if f is not None:
-        _require(f, "f", torch.float64)
-    ws = plan._ws(OP_GRAD, B, blur=blur, ws=ws)
+        _adopt(stream, out)
+    _require(out, "g", plan.torch_dtype, (plan.p_alloc,))
+    _same_batch(B, (b, "b", 2), (out, "g", 1))
+    _check_f(f, B)
+    ws = plan._ws(OP_GRAD, B, blur=blur, ws=ws, stream=stream)
     if adjoint == "true":
         _check(lib().wl_grad(plan._h, blur._h, B, _ptr(x), _ptr(b), _ptr(out), _ptr(f), _ptr(ws),
                              _stream_ptr(stream)))
@@ -436,11 +481,6 @@ class Graph:
 
 
 # ------------------------------------------------------------------ FISTA
-def next_t(t: float) -> float:
-    """FISTA momentum recursion t_{k+1} = (1 + sqrt(1 + 4 t_k^2)) / 2 (host scalar)."""
-    return (1.0 + (1.0 + 4.0 * t * t) ** 0.5) / 2.0
-
-
 def lipschitz(plan: Plan, blur: Blur, iters: int = 50, seed: int = 1, ws=None, stream=None) -> float:
     """lambda_max(W* R* R W) by power iteration on the GPU (wl_lipschitz; blocking)."""
     ws = plan._ws(OP_LIPSCHITZ, 1, blur=blur, ws=ws)
@@ -455,9 +495,11 @@ def fista_update(plan: Plan, g, x, y, t: float, lam: float, lip: float, stream=N
     for name, a in (("g", g), ("x", x), ("y", y)):
         _require(a, name, plan.torch_dtype, (plan.p_alloc,))
     B = plan._batch_of(x, 1)
+    _same_batch(B, (g, "g", 1), (y, "y", 1))
+    t_next = ctypes.c_double()
     _check(lib().wl_fista_update(plan._h, B, _ptr(g), _ptr(x), _ptr(y), float(t), float(lam), float(lip),
-                                 _stream_ptr(stream)))
-    return next_t(t)
+                                 ctypes.byref(t_next), _stream_ptr(stream)))
+    return t_next.value
 
 
 def fista_step(plan: Plan, blur: Blur, b, x, y, t, lam: float, lip: float, f=None, ws=None, stream=None,
@@ -471,17 +513,18 @@ def fista_step(plan: Plan, blur: Blur, b, x, y, t, lam: float, lip: float, f=Non
     _require(x, "x", plan.torch_dtype, (plan.p_alloc,))
     _require(y, "y", plan.torch_dtype, (plan.p_alloc,))
     B = plan._batch_of(x, 1)
-    if f is not None:
-        _require(f, "f", _torch().float64)
-    ws = plan._ws(OP_FISTA, B, blur=blur, ws=ws)
+    _same_batch(B, (b, "b", 2), (y, "y", 1))
+    _check_f(f, B)
+    ws = plan._ws(OP_FISTA, B, blur=blur, ws=ws, stream=stream)
     if isinstance(t, _torch().Tensor):
         _require(t, "t", _torch().float64)
         _check(lib().wl_fista_step_dev(plan._h, blur._h, B, _ptr(b), _ptr(x), _ptr(y), _ptr(t), float(lam),
                                        float(lip), _ptr(f), ADJOINTS[adjoint], _ptr(ws), _stream_ptr(stream)))
         return t
+    t_next = ctypes.c_double()
     _check(lib().wl_fista_step(plan._h, blur._h, B, _ptr(b), _ptr(x), _ptr(y), float(t), float(lam), float(lip),
-                               _ptr(f), ADJOINTS[adjoint], _ptr(ws), _stream_ptr(stream)))
-    return next_t(t)
+                               _ptr(f), ADJOINTS[adjoint], _ptr(ws), ctypes.byref(t_next), _stream_ptr(stream)))
+    return t_next.value
 
 
 def fista(plan: Plan, blur: Blur, b, lam: float, iters: int, lip: float = None, x0=None, stream=None,
@@ -495,22 +538,31 @@ def fista(plan: Plan, blur: Blur, b, lam: float, iters: int, lip: float = None, 
         lip = lipschitz(plan, blur, stream=stream)
     x = torch.zeros(b.shape[:-2] + (plan.p_alloc,), dtype=b.dtype, device=b.device) if x0 is None else x0.clone()
     y = x.clone()
+    t_dev = torch.ones(1, dtype=torch.float64, device=b.device)
     ws = plan._ws(OP_FISTA, B, blur=blur)
+    cur = torch.cuda.current_stream()
+    run = stream if stream is not None else cur
+    # x, y, t_dev and ws were made on the current stream: `run` starts after them, and the caller's
+    # stream resumes after the last iteration (the returned x, y are safe to use there)
+    run.wait_stream(cur)
+    _adopt(run, x, y, t_dev, ws)
     iters = int(iters)
     if not graph:
         t = 1.0
         for _ in range(iters):
-            t = fista_step(plan, blur, b, x, y, t, lam, lip, ws=ws, stream=stream, adjoint=adjoint)
+            t = fista_step(plan, blur, b, x, y, t, lam, lip, ws=ws, stream=run, adjoint=adjoint)
+        cur.wait_stream(run)
         return x, y, t
-    t_dev = torch.ones(1, dtype=torch.float64, device=b.device)
     if iters == 0:
         return x, y, 1.0
-    step = lambda: fista_step(plan, blur, b, x, y, t_dev, lam, lip, ws=ws, adjoint=adjoint)  # noqa: E731
-    step()                                   # iteration 1, eager (warms every per-kernel cache)
-    if iters > 1:
-        g = Graph(step, warmup=0)
-        for _ in range(iters - 1):
-            g.replay()
+    with torch.cuda.stream(run):
+        step = lambda: fista_step(plan, blur, b, x, y, t_dev, lam, lip, ws=ws, adjoint=adjoint)  # noqa: E731
+        step()                                   # iteration 1, eager (warms every per-kernel cache)
+        if iters > 1:
+            g = Graph(step, warmup=0)
+            for _ in range(iters - 1):
+                g.replay()
+    cur.wait_stream(run)
     return x, y, float(t_dev.item())
 
 
@@ -543,7 +595,8 @@ def conv_full(h, s, out=None, stream=None):
         raise ValueError("h and s must have the same batch shape")
     if out is None:
         out = _torch().empty(h.shape[:-1] + (K + N - 1,), dtype=h.dtype, device=h.device)
-    _check_1d(out, "out", K + N - 1, h.dtype)
+    if _check_1d(out, "out", K + N - 1, h.dtype) != B:
+        raise ValueError("out must have the batch of h")
     _check(lib().wl_conv_full(_dtype_of(h), B, K, N, _ptr(h), _ptr(s), _ptr(out), _stream_ptr(stream)))
     return out
 
@@ -556,7 +609,8 @@ def conv_adjoint_h(s, r, K: int, out=None, stream=None):
         raise ValueError("s and r must have the same batch shape")
     if out is None:
         out = _torch().empty(s.shape[:-1] + (K,), dtype=s.dtype, device=s.device)
-    _check_1d(out, "out", K, s.dtype)
+    if _check_1d(out, "out", K, s.dtype) != B:
+        raise ValueError("out must have the batch of s")
     _check(lib().wl_conv_adjoint_h(_dtype_of(s), B, K, N, _ptr(s), _ptr(r), _ptr(out), _stream_ptr(stream)))
     return out
 
@@ -569,7 +623,8 @@ def conv_adjoint_s(h, r, N: int, out=None, stream=None):
         raise ValueError("h and r must have the same batch shape")
     if out is None:
         out = _torch().empty(h.shape[:-1] + (N,), dtype=h.dtype, device=h.device)
-    _check_1d(out, "out", N, h.dtype)
+    if _check_1d(out, "out", N, h.dtype) != B:
+        raise ValueError("out must have the batch of h")
     _check(lib().wl_conv_adjoint_s(_dtype_of(h), B, K, N, _ptr(h), _ptr(r), _ptr(out), _stream_ptr(stream)))
     return out
 
@@ -599,8 +654,9 @@ def bce_grad(h, s, x, lam_tv: float = 0.01, delta: float = 0.1, gh=None, gs=None
     gs = torch.empty_like(s) if gs is None else gs
     _check_1d(gh, "gh", K, h.dtype)
     _check_1d(gs, "gs", N, h.dtype)
-    if f is not None:
-        _require(f, "f", torch.float64)
+    if tuple(gh.shape) != tuple(h.shape) or tuple(gs.shape) != tuple(s.shape):
+        raise ValueError("gh / gs must be shaped like h / s")
+    _check_f(f, P)
     _check(lib().wl_bce_grad(_dtype_of(h), P, C, K, N, _ptr(h), _ptr(s), _ptr(x), shared, float(lam_tv),
                              float(delta), _ptr(gh), _ptr(gs), _ptr(f), _stream_ptr(stream)))
     return gh, gs

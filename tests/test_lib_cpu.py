@@ -140,9 +140,17 @@ def test_new_entry_points_validate_before_any_launch():
     assert L.wl_fista_step_dev(p._h, b._h, 1, vp(16), vp(32), vp(48), None, 0.1, 1.0, None, 0, None,
                                None) == wl.WL_EINVAL
     assert b"t_dev" in L.wl_last_error()
-    assert L.wl_fista_step(p._h, b._h, 1, vp(16), vp(32), vp(48), 0.5, 0.1, 1.0, None, 0, None,
+    assert L.wl_fista_step(p._h, b._h, 1, vp(16), vp(32), vp(48), 0.5, 0.1, 1.0, None, 0, None, None,
                            None) == wl.WL_EINVAL                                            # t < 1
-    assert L.wl_fista_update(p._h, 1, vp(16), vp(32), vp(48), 1.0, 0.1, 0.0, None) == wl.WL_EINVAL  # lip = 0
+    assert L.wl_fista_update(p._h, 1, vp(16), vp(32), vp(48), 1.0, 0.1, 0.0, None, None) == wl.WL_EINVAL  # lip = 0
+    # t_{k+1} comes back through the host out-pointer (batch 0: no launch, no device pointer needed)
+    tn = ctypes.c_double()
+    assert L.wl_fista_update(p._h, 0, None, None, None, 1.0, 0.1, 1.0, ctypes.byref(tn), None) == wl.WL_OK
+    assert tn.value == (1.0 + 5.0 ** 0.5) / 2.0
+    tn2 = ctypes.c_double()
+    assert L.wl_fista_step(p._h, b._h, 0, None, None, None, tn.value, 0.1, 1.0, None, 0, None, ctypes.byref(tn2),
+                           None) == wl.WL_OK
+    assert abs(tn2.value - (1.0 + (1.0 + 4.0 * tn.value ** 2) ** 0.5) / 2.0) < 1e-15
     # Example 2
     assert L.wl_bce_grad(0, 1, 2, 5, 9, vp(16), vp(32), vp(48), 0, 0.01, 0.0, vp(64), vp(80), None,
                          None) == wl.WL_EINVAL                                              # delta = 0
@@ -153,3 +161,14 @@ def test_new_entry_points_validate_before_any_launch():
     assert L.wl_conv_full(0, 1, 0, 9, vp(16), vp(32), vp(48), None) == wl.WL_ESIZE       # K = 0
     assert L.wl_conv_full(5, 1, 3, 9, vp(16), vp(32), vp(48), None) == wl.WL_EDTYPE      # bad dtype
     assert L.wl_conv_adjoint_h(0, 0, 3, 9, None, None, None, None) == wl.WL_OK           # empty batch
+
+
+def test_binding_batch_helpers():
+    """The binding's batch / f checks: pure metadata logic, checked on CPU tensors."""
+    import torch
+    wl._same_batch(4, (torch.zeros(4, 10), "x", 1), (torch.zeros(2, 2, 3, 3), "b", 2), (None, "f", 1))
+    with pytest.raises(ValueError, match="batch 1"):
+        wl._same_batch(4, (torch.zeros(1, 10), "b", 1))
+    with pytest.raises(ValueError, match="batch 3"):
+        wl._same_batch(1, (torch.zeros(3, 5, 5), "img", 2))
+    wl._same_batch(1, (torch.zeros(5, 5), "img", 2))              # no leading dims = batch 1
