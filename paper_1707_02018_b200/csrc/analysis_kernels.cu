@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "device_common.cuh"
 #include "wl_internal.h"
@@ -165,32 +166,25 @@ __device__ __forceinline__ void fista_pair(const AnaStreamParams<T, L> &p, T mom
   *reinterpret_cast<P *>(yp) = yn;
 }
 
+// One level's runs, handed to the CTAs of the grid (the body of k_ana_stream; k_ana_multi calls it
+// once per level of the coarse tail).  `phase` carries the stage barriers' parities across calls.
 template <typename T, int L, bool FU, int NS>
-__global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? 768 / ACfg<T, L, NS, FU>::NT : 1)
-    k_ana_stream(const __grid_constant__ AnaStreamParams<T, L> p) {
+__device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, unsigned char *smem_raw,
+                                               unsigned &phase) {
   using C = ACfg<T, L, NS, FU>;
   using P = typename C::P;
   using Vt = typename Vec16<T>::type;
   constexpr int G = C::G, GI = C::GI, VEC = C::VEC, V = C::V, VC = C::VC, TQ = C::TQ;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
   T *ubuf = reinterpret_cast<T *>(smem_raw + C::OFF_U);  // [NS][GI][UP] input rows
   T *hist = reinterpret_cast<T *>(smem_raw + C::OFF_H);  // [2][HR][HP] lo / hi coefficient columns
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + C::OFF_BAR);
   T *ftile = reinterpret_cast<T *>(smem_raw + C::OFF_F);  // FU only: [NS][4][2 (y, x)][G][TQ]
-
   const int tid = threadIdx.x;
-  if (tid == 0) {
-    for (int i = 0; i < C::NS; i++) mbar_init(bar + i, 1);
-  }
-  __syncthreads();
-  pdl_launch_dependents();
-  pdl_wait();  // the previous kernel of the stream wrote our inputs
   T mom = p.mom;
   if (FU && p.tdev) {
     const double t = *p.tdev, t_new = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
     mom = T((t - 1.0) / t_new);
   }
-  unsigned phase = 0;
   // B item: segment fastest; C item: column pair fastest, then set (lo / hi), then group
   const bool actB = tid < C::ITEMS_B;
   const int segB = tid % C::SEGB, rowB = tid / C::SEGB;
@@ -452,14 +446,67 @@ __global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? 768 /
   }
 }
 
+template <typename T, int L, bool FU, int NS>
+__global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? 768 / ACfg<T, L, NS, FU>::NT : 1)
+    k_ana_stream(const __grid_constant__ AnaStreamParams<T, L> p) {
+  using C = ACfg<T, L, NS, FU>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + C::OFF_BAR);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::NS; i++) mbar_init(bar + i, 1);
+  }
+  __syncthreads();
+  pdl_launch_dependents();
+  pdl_wait();  // the previous kernel of the stream wrote our inputs
+  unsigned phase = 0;
+  ana_level_runs<T, L, FU, NS>(p, smem_raw, phase);
+}
+
+// The coarse tail of a W* / W-dagger chain in one persistent launch: levels
+// j0 .. J one after another, separated by grid-wide barriers (cooperative launch: every CTA is
+// resident), so the short, latency-bound levels pay no kernel boundary each.
+constexpr int kMaxMulti = 12;
+template <typename T, int L>
+struct AnaMultiParams {
+  AnaStreamParams<T, L> lev[kMaxMulti];
+  int nlev;
+};
+
+template <typename T, int L>
+__global__ void __launch_bounds__(ACfg<T, L, 4, false>::NT, sizeof(T) == 4 ? 768 / ACfg<T, L, 4, false>::NT : 1)
+    k_ana_multi(const __grid_constant__ AnaMultiParams<T, L> mp) {
+  using C = ACfg<T, L, 4, false>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + C::OFF_BAR);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::NS; i++) mbar_init(bar + i, 1);
+  }
+  __syncthreads();
+  pdl_launch_dependents();
+  pdl_wait();
+  unsigned phase = 0;
+  for (int l = 0; l < mp.nlev; l++) {
+    if (l > 0) {
+      // level l-1 wrote LL_{l-1} with generic stores; level l reads it by TMA (async proxy)
+      grid_sync_all();
+      fence_proxy_async_all();
+    }
+    ana_level_runs<T, L, false, 4>(mp.lev[l], smem_raw, phase);
+  }
+}
+
 #ifndef WL_ANA_MINROWS
 #define WL_ANA_MINROWS 1  // minimum band height in units of G/2 coefficient rows (A/B on B200: 1 beat 2, cfg4 W* -7 %)
 #endif
 
+// Fill the launch parameters of one level.  short_run (out): the level's bands are at most
+// short_run_max(3) blocks, so it runs the 4-stage variant (NS = 4); force_short: build the NS = 4
+// configuration regardless (levels of k_ana_multi), with `resident4` CTAs sharing the runs.
 template <typename T, int L, bool FU>
-cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
+cudaError_t make_ana_params(const AnalysisArgs &a, AnaStreamParams<T, L> &p, bool &short_run, bool force_short,
+                            long long resident4 = 0) {
   using C = ACfg<T, L, 0, FU>;
-  AnaStreamParams<T, L> p;
+  using C4 = ACfg<T, L, 4, FU>;
   memset(&p, 0, sizeof p);
   p.in = static_cast<const T *>(a.in);
   p.in_pitch = a.in_pitch;
@@ -497,27 +544,96 @@ cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
   p.mom = T(a.fista_mom);
   p.tdev = a.fista_tdev;
   p.nstrips = (a.m1 + C::TQ - 1) / C::TQ;
-  // runs of at most 3 blocks (coarse levels) prefetch all their blocks at once (NS = 4)
   long long resident = 0;
-  cudaError_t e = kernel_resident(reinterpret_cast<const void *>(k_ana_stream<T, L, FU, 0>), C::NT,
-                                  C::smem_bytes(FU), &resident);
-  if (e != cudaSuccess) return e;
-  p.runs = RunMap::make((long long)a.batch * p.nstrips, a.m0, resident, std::max(1, C::G * WL_ANA_MINROWS / 2), 1);
-  const int band = (a.m0 + p.runs.nb_lo - 1) / p.runs.nb_lo;
-  if ((band + C::G - 1) / C::G <= short_run_max(3)) {
-    using C4 = ACfg<T, L, 4, FU>;
-    e = kernel_resident(reinterpret_cast<const void *>(k_ana_stream<T, L, FU, 4>), C4::NT, C4::smem_bytes(FU),
+  cudaError_t e;
+  if (force_short) {
+    short_run = true;
+  } else {
+    // runs of at most 3 blocks (coarse levels) prefetch all their blocks at once (NS = 4)
+    e = kernel_resident(reinterpret_cast<const void *>(k_ana_stream<T, L, FU, 0>), C::NT, C::smem_bytes(FU),
                         &resident);
     if (e != cudaSuccess) return e;
-    p.runs = RunMap::make((long long)a.batch * p.nstrips, a.m0, resident, std::max(1, C4::G * WL_ANA_MINROWS / 2), 1);
+    p.runs = RunMap::make((long long)a.batch * p.nstrips, a.m0, resident, std::max(1, C::G * WL_ANA_MINROWS / 2), 1);
+    const int band = (a.m0 + p.runs.nb_lo - 1) / p.runs.nb_lo;
+    short_run = (band + C::G - 1) / C::G <= short_run_max(3);
+  }
+  if (short_run) {
+    if (!force_short) {
+      e = kernel_resident(reinterpret_cast<const void *>(k_ana_stream<T, L, FU, 4>), C4::NT, C4::smem_bytes(FU),
+                          &resident4);
+      if (e != cudaSuccess) return e;
+    }
+    p.runs = RunMap::make((long long)a.batch * p.nstrips, a.m0, resident4, std::max(1, C4::G * WL_ANA_MINROWS / 2), 1);
     encode(C4::UW, C4::GI);
+  } else {
+    encode(C::UW, C::GI);
+  }
+  return cudaSuccess;
+}
+
+template <typename T, int L, bool FU>
+cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
+  using C = ACfg<T, L, 0, FU>;
+  using C4 = ACfg<T, L, 4, FU>;
+  AnaStreamParams<T, L> p;
+  bool short_run = false;
+  cudaError_t e = make_ana_params<T, L, FU>(a, p, short_run, false);
+  if (e != cudaSuccess) return e;
+  long long resident = 0;
+  if (short_run) {
+    e = kernel_resident(reinterpret_cast<const void *>(k_ana_stream<T, L, FU, 4>), C4::NT, C4::smem_bytes(FU), &resident);
+    if (e != cudaSuccess) return e;
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
     e = launch_pdl(k_ana_stream<T, L, FU, 4>, grid, C4::NT, C4::smem_bytes(FU), s, p, 'a');
   } else {
-    encode(C::UW, C::GI);
+    e = kernel_resident(reinterpret_cast<const void *>(k_ana_stream<T, L, FU, 0>), C::NT, C::smem_bytes(FU), &resident);
+    if (e != cudaSuccess) return e;
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
     e = launch_pdl(k_ana_stream<T, L, FU, 0>, grid, C::NT, C::smem_bytes(FU), s, p, 'A');
   }
+  g_launches++;
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+// A whole W* / W-dagger chain: the long levels one launch each, the short coarse tail (>= 2
+// levels) as one cooperative k_ana_multi launch (only with WL_MULTI: per-level PDL launches measured faster).
+template <typename T, int L>
+cudaError_t launch_ana_chain_t(const AnalysisArgs *a, int n, cudaStream_t s) {
+  using C4 = ACfg<T, L, 4, false>;
+  int first_short = n;
+  for (int i = 0; i < n && first_short == n; i++) {
+    AnaStreamParams<T, L> p;
+    bool sr = false;
+    cudaError_t e = make_ana_params<T, L, false>(a[i], p, sr, false);
+    if (e != cudaSuccess) return e;
+    if (sr) first_short = i;
+  }
+  const int nmulti = multi_enabled() ? std::min(n - first_short, kMaxMulti) : 0;
+  const int nsingle = nmulti >= 2 ? n - nmulti : n;
+  for (int i = 0; i < nsingle; i++) {
+    cudaError_t e = launch_ana_stream_t<T, L, false>(a[i], s);
+    if (e != cudaSuccess) return e;
+  }
+  if (nsingle == n) return cudaSuccess;
+  long long resident = 0;
+  cudaError_t e = kernel_resident(reinterpret_cast<const void *>(k_ana_multi<T, L>), C4::NT, C4::smem_bytes(false),
+                                  &resident);
+  if (e != cudaSuccess) return e;
+  static AnaMultiParams<T, L> mp;  // large: not on the host stack; launches copy it
+  static std::mutex mu;
+  std::lock_guard<std::mutex> g(mu);
+  memset(&mp, 0, sizeof mp);
+  mp.nlev = n - nsingle;
+  long long maxruns = 0;
+  for (int l = 0; l < mp.nlev; l++) {
+    bool sr = true;
+    e = make_ana_params<T, L, false>(a[nsingle + l], mp.lev[l], sr, true, resident);
+    if (e != cudaSuccess) return e;
+    maxruns = std::max<long long>(maxruns, mp.lev[l].runs.nruns());
+  }
+  const int grid = (int)std::min<long long>(maxruns, resident);
+  e = launch_coop(k_ana_multi<T, L>, grid, C4::NT, C4::smem_bytes(false), s, mp);
   g_launches++;
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
@@ -542,7 +658,24 @@ cudaError_t dispatch(const AnalysisArgs &a, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
+template <typename T>
+cudaError_t dispatch_chain(const AnalysisArgs *a, int n, cudaStream_t s) {
+  switch (a[0].L) {
+    case 2: return launch_ana_chain_t<T, 2>(a, n, s);
+    case 4: return launch_ana_chain_t<T, 4>(a, n, s);
+    case 8: return launch_ana_chain_t<T, 8>(a, n, s);
+    case 10: return launch_ana_chain_t<T, 10>(a, n, s);
+    case 16: return launch_ana_chain_t<T, 16>(a, n, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 }  // namespace
+
+cudaError_t launch_analysis_chain(int dtype, const AnalysisArgs *a, int n, cudaStream_t s) {
+  if (n <= 0 || a[0].batch == 0) return cudaSuccess;
+  return dtype == WL_F64 ? dispatch_chain<double>(a, n, s) : dispatch_chain<float>(a, n, s);
+}
 
 cudaError_t launch_analysis(int dtype, const AnalysisArgs &a, cudaStream_t s) {
   if (a.batch == 0 || a.m0 == 0 || a.m1 == 0) return cudaSuccess;

@@ -181,8 +181,10 @@ wl_status run_analysis(const wl_plan *p, int64_t batch, const void *img, void *x
     ext = p->bc == WL_BC_PERIODIC ? EXT_PER : (p->bc == WL_BC_SYMMETRIC_EDAG ? EXT_SYM_PADJ : EXT_ZERO);
   else
     ext = p->bc == WL_BC_PERIODIC ? EXT_PER : (p->bc == WL_BC_ZERO ? EXT_ZERO : EXT_SYM);
+  AnalysisArgs chain[WL_MAX_LEVELS];
   for (int j = 1; j <= p->J; j++) {
-    AnalysisArgs a;
+    AnalysisArgs &a = chain[j - 1];
+    a = AnalysisArgs();
     if (j == 1) {
       a.in = img;
       a.in_pitch = p->w;
@@ -218,9 +220,13 @@ wl_status run_analysis(const wl_plan *p, int64_t batch, const void *img, void *x
       a.fista_tau = fz->tau;
       a.fista_mom = fz->mom;
       a.fista_tdev = fz->tdev;
+      cudaError_t e = launch_analysis(p->dtype, a, s);
+      if (e != cudaSuccess) return cuda_fail(e, "analysis level launch");
     }
-    cudaError_t e = launch_analysis(p->dtype, a, s);
-    if (e != cudaSuccess) return cuda_fail(e, "analysis level launch");
+  }
+  if (!fz) {  // long levels one launch each, the short coarse tail as one persistent launch
+    cudaError_t e = launch_analysis_chain(p->dtype, chain, p->J, s);
+    if (e != cudaSuccess) return cuda_fail(e, "analysis chain launch");
   }
   return WL_OK;
 }
@@ -233,8 +239,10 @@ wl_status run_synthesis(const wl_plan *p, int64_t batch, const void *x, void *im
                         cudaStream_t s, bool transpose_of_analysis = false) {
   const int Lp = p->fb.L - 1;
   const bool sym = p->bc == WL_BC_SYMMETRIC_EDAG || (transpose_of_analysis && p->bc == WL_BC_SYMMETRIC);
+  SynthesisArgs chain[WL_MAX_LEVELS];  // coarse -> fine, launched together when no fold interleaves
   for (int j = p->J; j >= 1; j--) {
-    SynthesisArgs a;
+    SynthesisArgs &a = chain[p->J - j];
+    a = SynthesisArgs();
     Buf ll = (j == p->J) ? band_buf(p, x, 0) : ll_buf(p, ws, L, j);
     Buf bands[4] = {ll, band_buf(p, x, lh_index(p, j)), band_buf(p, x, lh_index(p, j) + 1),
                     band_buf(p, x, lh_index(p, j) + 2)};
@@ -294,9 +302,11 @@ wl_status run_synthesis(const wl_plan *p, int64_t batch, const void *x, void *im
       a.N1 = (int)n1;
       a.o0 = 0;
       a.o1 = 0;
-      cudaError_t e = launch_synthesis(p->dtype, a, s);
-      if (e != cudaSuccess) return cuda_fail(e, "synthesis level launch");
     }
+  }
+  if (!sym) {  // the short coarse head as one persistent launch, then the long levels
+    cudaError_t e = launch_synthesis_chain(p->dtype, chain, p->J, s);
+    if (e != cudaSuccess) return cuda_fail(e, "synthesis chain launch");
   }
   return WL_OK;
 }

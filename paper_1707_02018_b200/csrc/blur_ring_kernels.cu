@@ -138,34 +138,6 @@ __device__ __forceinline__ unsigned ring_box_bytes(bool inside, int G, int c_sta
   return (unsigned)(G * (inside ? c_width : n) * 4);
 }
 
-// u columns [-HW, 0) and [w, w + HW) of the G rows of one stage <- their mirror images (in both
-// boxes where present).  Edge strips only; out of line to keep the step loop small.
-template <int HW, bool RESID>
-__device__ __noinline__ void ring_fix_u(float *ust, int ustart, int w, int tid) {
-  using C = RingCfg<HW, RESID>;
-  for (int idx = tid; idx < C::G * 2 * HW; idx += C::NT) {
-    const int r = idx / (2 * HW), j = idx - r * (2 * HW);
-    const int c = j < HW ? j - HW : w + j - HW, x = c - ustart;
-    if (x < 0 || x >= 128 + C::UBOX) continue;
-    const int sx = refl_inf(c, w) - ustart;
-    const float v = sx < C::UBOX ? ust[r * C::UBOX + sx] : ust[C::UREG + r * C::UBOX + sx - 128];
-    if (x < C::UBOX) ust[r * C::UBOX + x] = v;
-    if (x >= 128) ust[C::UREG + r * C::UBOX + x - 128] = v;
-  }
-}
-
-// r columns [-HW, 0) and [w, w + HW) of one r row block <- their mirror images.
-template <int HW, bool RESID>
-__device__ __noinline__ void ring_fix_r(float *rw, int col1, int w, int tid) {
-  using C = RingCfg<HW, RESID>;
-  for (int idx = tid; idx < C::G * 2 * HW; idx += C::NT) {
-    const int r = idx / (2 * HW), j = idx - r * (2 * HW);
-    const int c = j < HW ? j - HW : w + j - HW, x = c - col1;
-    if (x < 0 || x >= C::NC) continue;
-    rw[r * C::NC + x] = rw[r * C::NC + refl_inf(c, w) - col1];
-  }
-}
-
 __device__ __forceinline__ void st_pair_if(float *ptr, float2 v, bool pred) {
   asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %3, 0;\n @p st.global.v2.f32 [%0], {%1, %2};\n}\n" ::"l"(ptr),
                "f"(v.x), "f"(v.y), "r"((int)pred)
@@ -233,8 +205,30 @@ __global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_co
     const int brow0 = urow0 - HW;            // b / r row of step 0 (residual)
     // strips whose u / r rows reach past an image edge mirror the HW columns beyond it in shared
     // memory (u and r are symmetric about the edges for a symmetric PSF), once per group
-    const bool uedge = ustart < 0 || ustart + 128 + C::UBOX > w;
-    const bool redge = RESID && (col1 < 0 || col1 + C::NC > w);
+    // Edge strips: the HW image columns beyond an edge, [-HW, 0) and [w, w + HW), are overwritten
+    // in shared memory with their mirror images (u and r are symmetric about the edges for a
+    // symmetric PSF) before a horizontal pass reads them.  Lane j < 2HW of each warp owns edge
+    // column j: when it lies in the warp's read range, the lane copies its source column row by
+    // row (offsets fixed per run) and the warp syncs itself; overlapping warps write equal values.
+    const int lane = tid & 31, wq = (tid >> 5) * 64;
+    int ufix_t = -1, ufix_s = 0, rfix_t = -1, rfix_s = 0;
+    if (lane < 2 * HW) {
+      const int c = lane < HW ? lane - HW : w + lane - HW;  // the edge column of this lane
+      const int x = c - ustart;                              // its u index over [0, 128 + UBOX)
+      const int ulo = wq + (col1 - HW - ustart) - S0;        // this warp's u read range
+      if (x >= ulo && x < ulo + 62 + NWIN && x >= box * 128 && x < box * 128 + C::UBOX) {
+        const int sx = refl_inf(c, w) - ustart;
+        ufix_t = box * C::UREG + x - box * 128;
+        ufix_s = sx < C::UBOX ? sx : C::UREG + sx - 128;
+      }
+      const int xr = c - col1;                               // its r index over [0, NC)
+      if (RESID && xr >= wq && xr < wq + 62 + NWIN && xr < C::NC) {
+        rfix_t = xr;
+        rfix_s = refl_inf(c, w) - col1;
+      }
+    }
+    const bool uedge = __any_sync(0xffffffffu, ufix_t >= 0);
+    const bool redge = RESID && __any_sync(0xffffffffu, rfix_t >= 0);
     const int widx = box * C::UREG + 2 * tid + (col1 - HW - ustart) - S0 - box * 128;  // even
     const int bidx = box * C::BREG + 2 * tid + (col1 - bstart) - box * 128;
     // output pair columns (c0 + 2 tid, +1)
@@ -286,8 +280,11 @@ __global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_co
         mbar_wait(full + st, (g / S) & 1);
         float *ust = ubase + st * 2 * C::UREG;
         if (uedge) {
-          ring_fix_u<HW, RESID>(ust, ustart, w, tid);
-          __syncthreads();
+          if (ufix_t >= 0) {
+#pragma unroll
+            for (int r = 0; r < G; r++) ust[r * C::UBOX + ufix_t] = ust[r * C::UBOX + ufix_s];
+          }
+          __syncwarp();
         }
         const float *ub = ust + widx;
         const float *bb = bbase + st * 2 * C::BREG + bidx;
@@ -333,8 +330,11 @@ __global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_co
         // groups whose steps all precede 2HW only prime ring1 (their r rows feed no output)
         if (RESID && (k + 1) * G > 2 * HW) {
           if (redge) {
-            ring_fix_r<HW, RESID>(rw, col1, w, tid);
-            __syncthreads();
+            if (rfix_t >= 0) {
+#pragma unroll
+              for (int r = 0; r < G; r++) rw[r * C::NC + rfix_t] = rw[r * C::NC + rfix_s];
+            }
+            __syncwarp();
           }
           // ---------------- stage 2: h2 = R_h r -> ring2; s = R_v h2
           const float2 *rsrc = reinterpret_cast<const float2 *>(rw + 2 * tid);

@@ -1,5 +1,6 @@
 // Small device helpers shared by the libwl kernels (sm_100a).
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -149,6 +150,12 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const void *tmap, uint64_
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
       : "memory");
 }
+
+// Grid-wide barrier of a cooperative launch (gpu-scope fence included).
+__device__ __forceinline__ void grid_sync_all() { cooperative_groups::this_grid().sync(); }
+// Order this thread's earlier generic-proxy accesses (any state space) before its later
+// async-proxy (TMA) accesses: after a grid barrier, before TMA reads of data other CTAs stored.
+__device__ __forceinline__ void fence_proxy_async_all() { asm volatile("fence.proxy.async;\n" ::: "memory"); }
 
 // 1-D bulk copy global -> shared (16-byte aligned, bytes % 16 == 0); completion on `bar`.
 __device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes, uint64_t *bar) {

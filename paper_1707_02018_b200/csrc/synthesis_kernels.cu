@@ -27,6 +27,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "device_common.cuh"
 #include "wl_internal.h"
@@ -100,27 +101,20 @@ struct SynStreamParams {
   P e_hi[H_MAX], o_hi[H_MAX];
 };
 
+// One level's runs (the body of k_synth_stream; k_synth_multi calls it once per level of the
+// coarse head of a W chain).  `phase` carries the stage barriers' parities across calls.
 template <typename T, int L, int NS>
-__global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 768 / SCfg<T, L>::NT : 1)
-    k_synth_stream(const __grid_constant__ SynStreamParams<T, L> p) {
+__device__ __forceinline__ void syn_level_runs(const SynStreamParams<T, L> &p, unsigned char *smem_raw,
+                                               unsigned &phase) {
   using C = SCfg<T, L, NS>;
   using P = typename C::P;
   using Vt = typename Vec16<T>::type;
   constexpr int G = C::G, H = C::H, VEC = C::VEC, VC = C::VC, SP = C::SP;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
   T *cbuf = reinterpret_cast<T *>(smem_raw + C::OFF_C);  // [NS][4][G][KCP] coefficient windows
   T *vl = reinterpret_cast<T *>(smem_raw + C::OFF_V);    // [HR][TWP] VL history (rows s)
   T *vh = vl + C::HR * C::TWP;                           // [HR][TWP] VH history
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + C::OFF_BAR);
-
   const int tid = threadIdx.x;
-  if (tid == 0) {
-    for (int i = 0; i < C::NS; i++) mbar_init(bar + i, 1);
-  }
-  __syncthreads();
-  pdl_launch_dependents();
-  pdl_wait();  // the previous kernel of the stream wrote our inputs
-  unsigned phase = 0;
   // S1 item: segment fastest; S0 item: column pair fastest
   const bool act1 = tid < C::ITEMS1;
   const int seg1 = tid % C::NSEG, row1 = tid / C::NSEG;
@@ -334,15 +328,65 @@ __global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 768 / SCfg<T,
   }
 }
 
+template <typename T, int L, int NS>
+__global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 768 / SCfg<T, L>::NT : 1)
+    k_synth_stream(const __grid_constant__ SynStreamParams<T, L> p) {
+  using C = SCfg<T, L, NS>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + C::OFF_BAR);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::NS; i++) mbar_init(bar + i, 1);
+  }
+  __syncthreads();
+  pdl_launch_dependents();
+  pdl_wait();  // the previous kernel of the stream wrote our inputs
+  unsigned phase = 0;
+  syn_level_runs<T, L, NS>(p, smem_raw, phase);
+}
+
+// The coarse head of a W chain (levels J .. j0, coarse -> fine) in one persistent cooperative
+// launch with grid-wide barriers between the levels.
+constexpr int kMaxMulti = 12;
+template <typename T, int L>
+struct SynMultiParams {
+  SynStreamParams<T, L> lev[kMaxMulti];
+  int nlev;
+};
+
+template <typename T, int L>
+__global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 768 / SCfg<T, L>::NT : 1)
+    k_synth_multi(const __grid_constant__ SynMultiParams<T, L> mp) {
+  using C = SCfg<T, L, 4>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + C::OFF_BAR);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::NS; i++) mbar_init(bar + i, 1);
+  }
+  __syncthreads();
+  pdl_launch_dependents();
+  pdl_wait();
+  unsigned phase = 0;
+  for (int l = 0; l < mp.nlev; l++) {
+    if (l > 0) {
+      grid_sync_all();          // level l-1 stored LL with generic stores ...
+      fence_proxy_async_all();  // ... level l reads it by TMA (async proxy)
+    }
+    syn_level_runs<T, L, 4>(mp.lev[l], smem_raw, phase);
+  }
+}
+
 #ifndef WL_SYN_MINROWS
 #define WL_SYN_MINROWS 1  // minimum band height in units of G output rows (A/B on B200: 1 beat 2 on every small config)
 #endif
 
+// Fill the launch parameters of one level; short_run (out): bands of at most short_run_max(2)
+// batches run the 4-stage variant; force_short: NS = 4 with `resident4` CTAs (k_synth_multi levels).
 template <typename T, int L>
-cudaError_t launch_synth_stream_t(const SynthesisArgs &a, cudaStream_t s) {
+cudaError_t make_syn_params(const SynthesisArgs &a, SynStreamParams<T, L> &p, bool &short_run, bool force_short,
+                            long long resident4 = 0) {
   using C = SCfg<T, L>;
+  using C4 = SCfg<T, L, 4>;
   static_assert(C::H <= H_MAX, "H_MAX");
-  SynStreamParams<T, L> p;
   memset(&p, 0, sizeof p);
   const bool tma_ok = tma_enabled();  // WL_NO_TMA: debugging / A-B switch
   for (int i = 0; i < 4; i++) {
@@ -380,30 +424,101 @@ cudaError_t launch_synth_stream_t(const SynthesisArgs &a, cudaStream_t s) {
   const int span0 = a.o0 + a.N0 - p.t00, span1 = a.o1 + a.N1 - p.t01;
   p.nstrips = (span1 + C::TW - 1) / C::TW;
   long long resident = 0;
-  cudaError_t e = kernel_resident(reinterpret_cast<const void *>(k_synth_stream<T, L, 0>), C::NT, C::smem_bytes(),
-                                  &resident);
-  if (e != cudaSuccess) return e;
-  // one run per resident CTA when the columns allow it; even bands of >= 4 iterations
-  p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident, WL_SYN_MINROWS * C::G, 2);
-  const int band = (span0 + p.runs.nb_lo - 1) / p.runs.nb_lo;
-  if ((band / 2 + C::H - 1) / C::G + 1 <= short_run_max(2)) {
-    // short runs (coarse levels): every batch of the run in flight at once
-    using C4 = SCfg<T, L, 4>;
-    e = kernel_resident(reinterpret_cast<const void *>(k_synth_stream<T, L, 4>), C4::NT, C4::smem_bytes(),
-                        &resident);
+  cudaError_t e;
+  if (force_short) {
+    short_run = true;
+  } else {
+    e = kernel_resident(reinterpret_cast<const void *>(k_synth_stream<T, L, 0>), C::NT, C::smem_bytes(), &resident);
     if (e != cudaSuccess) return e;
-    p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident, WL_SYN_MINROWS * C4::G, 2);
+    // one run per resident CTA when the columns allow it; even bands of >= 4 iterations
+    p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident, WL_SYN_MINROWS * C::G, 2);
+    const int band = (span0 + p.runs.nb_lo - 1) / p.runs.nb_lo;
+    short_run = (band / 2 + C::H - 1) / C::G + 1 <= short_run_max(2);
+  }
+  if (short_run) {
+    // short runs (coarse levels): every batch of the run in flight at once
+    if (!force_short) {
+      e = kernel_resident(reinterpret_cast<const void *>(k_synth_stream<T, L, 4>), C4::NT, C4::smem_bytes(),
+                          &resident4);
+      if (e != cudaSuccess) return e;
+    }
+    p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident4, WL_SYN_MINROWS * C4::G, 2);
     encode(C4::KCW, C4::G);
+  } else {
+    encode(C::KCW, C::G);
+  }
+  return cudaSuccess;
+}
+
+template <typename T, int L>
+cudaError_t launch_synth_stream_t(const SynthesisArgs &a, cudaStream_t s) {
+  using C = SCfg<T, L>;
+  using C4 = SCfg<T, L, 4>;
+  SynStreamParams<T, L> p;
+  bool short_run = false;
+  cudaError_t e = make_syn_params<T, L>(a, p, short_run, false);
+  if (e != cudaSuccess) return e;
+  long long resident = 0;
+  if (short_run) {
+    e = kernel_resident(reinterpret_cast<const void *>(k_synth_stream<T, L, 4>), C4::NT, C4::smem_bytes(), &resident);
+    if (e != cudaSuccess) return e;
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
     e = launch_pdl(k_synth_stream<T, L, 4>, grid, C4::NT, C4::smem_bytes(), s, p, 's');
   } else {
-    encode(C::KCW, C::G);
+    e = kernel_resident(reinterpret_cast<const void *>(k_synth_stream<T, L, 0>), C::NT, C::smem_bytes(), &resident);
+    if (e != cudaSuccess) return e;
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
     e = launch_pdl(k_synth_stream<T, L, 0>, grid, C::NT, C::smem_bytes(), s, p, 'S');
   }
   g_launches++;
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+// A whole W chain given coarse -> fine (a[0] = level J): its short head (>= 2 levels) as one
+// cooperative k_synth_multi launch, then the long levels one launch each (only with WL_MULTI: per-level PDL launches measured faster).
+template <typename T, int L>
+cudaError_t launch_syn_chain_t(const SynthesisArgs *a, int n, cudaStream_t s) {
+  using C4 = SCfg<T, L, 4>;
+  int nshort = 0;  // coarse levels are short first: count the leading short ones
+  for (int i = 0; i < n; i++) {
+    SynStreamParams<T, L> p;
+    bool sr = false;
+    cudaError_t e = make_syn_params<T, L>(a[i], p, sr, false);
+    if (e != cudaSuccess) return e;
+    if (!sr) break;
+    nshort++;
+  }
+  const int nmulti = (multi_enabled() && nshort >= 2) ? std::min(nshort, kMaxMulti) : 0;
+  if (nmulti) {
+    long long resident = 0;
+    cudaError_t e = kernel_resident(reinterpret_cast<const void *>(k_synth_multi<T, L>), C4::NT, C4::smem_bytes(),
+                                    &resident);
+    if (e != cudaSuccess) return e;
+    static SynMultiParams<T, L> mp;  // large: not on the host stack; launches copy it
+    static std::mutex mu;
+    std::lock_guard<std::mutex> g(mu);
+    memset(&mp, 0, sizeof mp);
+    mp.nlev = nmulti;
+    long long maxruns = 0;
+    for (int l = 0; l < nmulti; l++) {
+      bool sr = true;
+      e = make_syn_params<T, L>(a[l], mp.lev[l], sr, true, resident);
+      if (e != cudaSuccess) return e;
+      maxruns = std::max<long long>(maxruns, mp.lev[l].runs.nruns());
+    }
+    const int grid = (int)std::min<long long>(maxruns, resident);
+    e = launch_coop(k_synth_multi<T, L>, grid, C4::NT, C4::smem_bytes(), s, mp);
+    g_launches++;
+    if (e != cudaSuccess) return e;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  for (int i = nmulti; i < n; i++) {
+    cudaError_t e = launch_synth_stream_t<T, L>(a[i], s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 template <typename T>
@@ -418,7 +533,24 @@ cudaError_t dispatch(const SynthesisArgs &a, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
+template <typename T>
+cudaError_t dispatch_chain(const SynthesisArgs *a, int n, cudaStream_t s) {
+  switch (a[0].L) {
+    case 2: return launch_syn_chain_t<T, 2>(a, n, s);
+    case 4: return launch_syn_chain_t<T, 4>(a, n, s);
+    case 8: return launch_syn_chain_t<T, 8>(a, n, s);
+    case 10: return launch_syn_chain_t<T, 10>(a, n, s);
+    case 16: return launch_syn_chain_t<T, 16>(a, n, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 }  // namespace
+
+cudaError_t launch_synthesis_chain(int dtype, const SynthesisArgs *a, int n, cudaStream_t s) {
+  if (n <= 0 || a[0].batch == 0) return cudaSuccess;
+  return dtype == WL_F64 ? dispatch_chain<double>(a, n, s) : dispatch_chain<float>(a, n, s);
+}
 
 cudaError_t launch_synthesis(int dtype, const SynthesisArgs &a, cudaStream_t s) {
   if (a.batch == 0 || a.N0 == 0 || a.N1 == 0) return cudaSuccess;

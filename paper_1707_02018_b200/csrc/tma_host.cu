@@ -71,6 +71,13 @@ bool tma_enabled() {
   return v;
 }
 
+bool multi_enabled() {
+  // measured on B200 (graph replay): the cooperative multi-level tail lost to per-level PDL
+  // launches (cfg4 W* 96 vs 80 us, cfg2 W* 26 vs 17 us): off unless WL_MULTI is set
+  static const bool v = getenv("WL_MULTI") != nullptr;
+  return v;
+}
+
 bool pdl_enabled(char kind) {
   static const char *off = [] {
     // measured on B200 (cfg5 grad -1.3 %, cfg3 grad -2.7 %, cfg4 W* neutral): the long blur and

@@ -79,7 +79,13 @@ struct BlurArgs {
 };
 
 cudaError_t launch_analysis(int dtype, const AnalysisArgs &a, cudaStream_t s);
+// A full chain of n analysis levels (fine -> coarse): the short coarse tail runs as one persistent
+// cooperative launch (k_ana_multi) with grid-wide barriers between its levels.
+cudaError_t launch_analysis_chain(int dtype, const AnalysisArgs *a, int n, cudaStream_t s);
 cudaError_t launch_synthesis(int dtype, const SynthesisArgs &a, cudaStream_t s);
+// A full chain of n synthesis levels given coarse -> fine: the short coarse head runs as one
+// persistent cooperative launch (k_synth_multi).
+cudaError_t launch_synthesis_chain(int dtype, const SynthesisArgs *a, int n, cudaStream_t s);
 cudaError_t launch_fold(int dtype, const FoldArgs &a, cudaStream_t s);
 cudaError_t launch_blur(int dtype, const BlurArgs &a, cudaStream_t s);
 cudaError_t launch_blur_residual(int dtype, const BlurArgs &a, cudaStream_t s);
@@ -145,6 +151,8 @@ int short_run_max(int dflt);
 
 // TMA loads unless WL_NO_TMA is set (debugging / A-B switch); read once per process
 bool tma_enabled();
+// multi-level persistent launches for the coarse tails only when WL_MULTI is set (A-B switch)
+bool multi_enabled();
 
 // PDL per launch site: kind 'A' / 'a' (analysis, long / short runs), 'S' / 's' (synthesis), 'b'
 // (blur).  WL_NO_PDL lists the kinds launched without it (an A/B switch; "AasSb" = none).
@@ -166,6 +174,31 @@ cudaError_t launch_pdl(Kern kern, int grid, int nt, size_t smem, cudaStream_t s,
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled(kind) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+// Cooperative launch (every CTA resident; grid-wide barriers allowed), with PDL when enabled for
+// kind 'm' (falls back to a plain cooperative launch if the combination is refused).
+template <typename Kern, typename Params>
+cudaError_t launch_coop(Kern kern, int grid, int nt, size_t smem, cudaStream_t s, const Params &p) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)nt);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled('m') ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
+  if (e != cudaSuccess && cfg.numAttrs == 2) {
+    cudaGetLastError();
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, p);
+  }
+  return e;
 }
 
 }  // namespace wl
