@@ -120,6 +120,22 @@ struct ACfg {
   }
 };
 
+// Structural zeros of the filter pair: the nonzero tap range [l0, l1) of the lowpass
+// and [h0, h1) of the highpass array of the L-tap frame.  ZV = 0: every tap; the CDF 9/7 frame
+// (reading R4: a_lo = [0, h9], d_lo = [0, 0, h7, 0], unified highpass rule) has zeros at both ends.
+template <int L, int ZV>
+struct TapRange {
+  static constexpr int l0 = 0, l1 = L, h0 = 0, h1 = L;
+};
+template <>
+struct TapRange<10, 1> {  // dual filters (d_lo, d_hi): W* and W
+  static constexpr int l0 = 2, l1 = 9, h0 = 0, h1 = 9;
+};
+template <>
+struct TapRange<10, 2> {  // analysis filters (a_lo, a_hi): W-dagger and (W-dagger)*
+  static constexpr int l0 = 1, l1 = 10, h0 = 1, h1 = 8;
+};
+
 template <typename T, int L>
 struct AnaStreamParams {
   using P = typename Pair<T>::t;
@@ -168,7 +184,7 @@ __device__ __forceinline__ void fista_pair(const AnaStreamParams<T, L> &p, T mom
 
 // One level's runs, handed to the CTAs of the grid (the body of k_ana_stream; k_ana_multi calls it
 // once per level of the coarse tail).  `phase` carries the stage barriers' parities across calls.
-template <typename T, int L, bool FU, int NS>
+template <typename T, int L, bool FU, int NS, int ZV = 0>
 __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, unsigned char *smem_raw,
                                                unsigned &phase) {
   using C = ACfg<T, L, NS, FU>;
@@ -342,8 +358,10 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
         P acc[V];
 #pragma unroll
         for (int k = 0; k < V; k++) acc[k] = zero2<P>();
+        using TR = TapRange<L, ZV>;
 #pragma unroll
         for (int j = L - 1; j >= 0; j--) {  // tap-outer, lowest window samples first (earliest loads)
+          if (j < (TR::l0 < TR::h0 ? TR::l0 : TR::h0) || j >= (TR::l1 > TR::h1 ? TR::l1 : TR::h1)) continue;
           const P f = p.fb[j];
 #pragma unroll
           for (int k = 0; k < V; k++) acc[k] = fma2(f, splat2<P>(win[C::SHIFT + 2 * k + L - 1 - j]), acc[k]);
@@ -373,13 +391,14 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
         P a0[VC], a1[VC];
 #pragma unroll
         for (int v = 0; v < VC; v++) a0[v] = a1[v] = zero2<P>();
+        using TRC = TapRange<L, ZV>;
 #pragma unroll
         for (int j = L - 1; j >= 0; j--) {
           const P fl = p.slo[j], fh = p.shi[j];
 #pragma unroll
           for (int v = 0; v < VC; v++) {
-            a0[v] = fma2(fl, win[2 * v + L - 1 - j], a0[v]);
-            a1[v] = fma2(fh, win[2 * v + L - 1 - j], a1[v]);
+            if (j >= TRC::l0 && j < TRC::l1) a0[v] = fma2(fl, win[2 * v + L - 1 - j], a0[v]);
+            if (j >= TRC::h0 && j < TRC::h1) a1[v] = fma2(fh, win[2 * v + L - 1 - j], a1[v]);
           }
         }
         // pitched rows: columns [m1, pitch) are padding written as 0; qc is even and so is
@@ -446,7 +465,7 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
   }
 }
 
-template <typename T, int L, bool FU, int NS>
+template <typename T, int L, bool FU, int NS, int ZV = 0>
 __global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? 768 / ACfg<T, L, NS, FU>::NT : 1)
     k_ana_stream(const __grid_constant__ AnaStreamParams<T, L> p) {
   using C = ACfg<T, L, NS, FU>;
@@ -459,7 +478,7 @@ __global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? 768 /
   pdl_launch_dependents();
   pdl_wait();  // the previous kernel of the stream wrote our inputs
   unsigned phase = 0;
-  ana_level_runs<T, L, FU, NS>(p, smem_raw, phase);
+  ana_level_runs<T, L, FU, NS, ZV>(p, smem_raw, phase);
 }
 
 // The coarse tail of a W* / W-dagger chain in one persistent launch: levels
@@ -571,7 +590,7 @@ cudaError_t make_ana_params(const AnalysisArgs &a, AnaStreamParams<T, L> &p, boo
   return cudaSuccess;
 }
 
-template <typename T, int L, bool FU>
+template <typename T, int L, bool FU, int ZV = 0>
 cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
   using C = ACfg<T, L, 0, FU>;
   using C4 = ACfg<T, L, 4, FU>;
@@ -581,15 +600,17 @@ cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   long long resident = 0;
   if (short_run) {
-    e = kernel_resident(reinterpret_cast<const void *>(k_ana_stream<T, L, FU, 4>), C4::NT, C4::smem_bytes(FU), &resident);
+    e = kernel_resident(reinterpret_cast<const void *>(k_ana_stream<T, L, FU, 4, ZV>), C4::NT, C4::smem_bytes(FU),
+                        &resident);
     if (e != cudaSuccess) return e;
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
-    e = launch_pdl(k_ana_stream<T, L, FU, 4>, grid, C4::NT, C4::smem_bytes(FU), s, p, 'a');
+    e = launch_pdl(k_ana_stream<T, L, FU, 4, ZV>, grid, C4::NT, C4::smem_bytes(FU), s, p, 'a');
   } else {
-    e = kernel_resident(reinterpret_cast<const void *>(k_ana_stream<T, L, FU, 0>), C::NT, C::smem_bytes(FU), &resident);
+    e = kernel_resident(reinterpret_cast<const void *>(k_ana_stream<T, L, FU, 0, ZV>), C::NT, C::smem_bytes(FU),
+                        &resident);
     if (e != cudaSuccess) return e;
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
-    e = launch_pdl(k_ana_stream<T, L, FU, 0>, grid, C::NT, C::smem_bytes(FU), s, p, 'A');
+    e = launch_pdl(k_ana_stream<T, L, FU, 0, ZV>, grid, C::NT, C::smem_bytes(FU), s, p, 'A');
   }
   g_launches++;
   if (e != cudaSuccess) return e;
@@ -598,7 +619,7 @@ cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
 
 // A whole W* / W-dagger chain: the long levels one launch each, the short coarse tail (>= 2
 // levels) as one cooperative k_ana_multi launch (only with WL_MULTI: per-level PDL launches measured faster).
-template <typename T, int L>
+template <typename T, int L, int ZV = 0>
 cudaError_t launch_ana_chain_t(const AnalysisArgs *a, int n, cudaStream_t s) {
   using C4 = ACfg<T, L, 4, false>;
   int first_short = n;
@@ -612,7 +633,7 @@ cudaError_t launch_ana_chain_t(const AnalysisArgs *a, int n, cudaStream_t s) {
   const int nmulti = multi_enabled() ? std::min(n - first_short, kMaxMulti) : 0;
   const int nsingle = nmulti >= 2 ? n - nmulti : n;
   for (int i = 0; i < nsingle; i++) {
-    cudaError_t e = launch_ana_stream_t<T, L, false>(a[i], s);
+    cudaError_t e = launch_ana_stream_t<T, L, false, ZV>(a[i], s);
     if (e != cudaSuccess) return e;
   }
   if (nsingle == n) return cudaSuccess;
@@ -639,20 +660,36 @@ cudaError_t launch_ana_chain_t(const AnalysisArgs *a, int n, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// Which TapRange matches the level's filter pair exactly (0: none, use every tap).
+int zero_variant(const AnalysisArgs &a) {
+  if (!zero_taps_enabled()) return 0;
+  return match_tap_range(a.lo, a.hi, a.L);
+}
+
 template <typename T>
 cudaError_t dispatch(const AnalysisArgs &a, cudaStream_t s) {
   if (a.fista_mask) switch (a.L) {
       case 2: return launch_ana_stream_t<T, 2, true>(a, s);
       case 4: return launch_ana_stream_t<T, 4, true>(a, s);
       case 8: return launch_ana_stream_t<T, 8, true>(a, s);
-      case 10: return launch_ana_stream_t<T, 10, true>(a, s);
+      case 10:
+        switch (zero_variant(a)) {
+          case 1: return launch_ana_stream_t<T, 10, true, 1>(a, s);
+          case 2: return launch_ana_stream_t<T, 10, true, 2>(a, s);
+          default: return launch_ana_stream_t<T, 10, true>(a, s);
+        }
       case 16: return launch_ana_stream_t<T, 16, true>(a, s);
     }
   else switch (a.L) {
       case 2: return launch_ana_stream_t<T, 2, false>(a, s);
       case 4: return launch_ana_stream_t<T, 4, false>(a, s);
       case 8: return launch_ana_stream_t<T, 8, false>(a, s);
-      case 10: return launch_ana_stream_t<T, 10, false>(a, s);
+      case 10:
+        switch (zero_variant(a)) {
+          case 1: return launch_ana_stream_t<T, 10, false, 1>(a, s);
+          case 2: return launch_ana_stream_t<T, 10, false, 2>(a, s);
+          default: return launch_ana_stream_t<T, 10, false>(a, s);
+        }
       case 16: return launch_ana_stream_t<T, 16, false>(a, s);
     }
   return cudaErrorInvalidValue;
@@ -664,7 +701,12 @@ cudaError_t dispatch_chain(const AnalysisArgs *a, int n, cudaStream_t s) {
     case 2: return launch_ana_chain_t<T, 2>(a, n, s);
     case 4: return launch_ana_chain_t<T, 4>(a, n, s);
     case 8: return launch_ana_chain_t<T, 8>(a, n, s);
-    case 10: return launch_ana_chain_t<T, 10>(a, n, s);
+    case 10:
+      switch (zero_variant(a[0])) {
+        case 1: return launch_ana_chain_t<T, 10, 1>(a, n, s);
+        case 2: return launch_ana_chain_t<T, 10, 2>(a, n, s);
+        default: return launch_ana_chain_t<T, 10>(a, n, s);
+      }
     case 16: return launch_ana_chain_t<T, 16>(a, n, s);
   }
   return cudaErrorInvalidValue;

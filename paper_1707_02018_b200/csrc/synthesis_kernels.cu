@@ -83,6 +83,23 @@ struct SCfg {
   static constexpr size_t smem_bytes() { return OFF_BAR + NS * sizeof(uint64_t); }
 };
 
+// Structural zeros of the filter pair: nonzero tap ranges [l0, l1) (lowpass) and
+// [h0, h1) (highpass) of the L-tap frame; ZV = 0: every tap (see analysis_kernels.cu TapRange).
+template <int L, int ZV>
+struct SynTaps {
+  static constexpr int l0 = 0, l1 = L, h0 = 0, h1 = L;
+};
+template <>
+struct SynTaps<10, 1> {  // CDF 9/7 dual filters (d_lo, d_hi): W
+  static constexpr int l0 = 2, l1 = 9, h0 = 0, h1 = 9;
+};
+template <>
+struct SynTaps<10, 2> {  // CDF 9/7 analysis filters (a_lo, a_hi): (W-dagger)*
+  static constexpr int l0 = 1, l1 = 10, h0 = 1, h1 = 8;
+};
+template <int A0, int A1>
+__host__ __device__ constexpr bool tap_in(int j) { return j >= A0 && j < A1; }
+
 template <typename T, int L>
 struct SynStreamParams {
   using P = typename Pair<T>::t;
@@ -103,7 +120,7 @@ struct SynStreamParams {
 
 // One level's runs (the body of k_synth_stream; k_synth_multi calls it once per level of the
 // coarse head of a W chain).  `phase` carries the stage barriers' parities across calls.
-template <typename T, int L, int NS>
+template <typename T, int L, int NS, int ZV = 0>
 __device__ __forceinline__ void syn_level_runs(const SynStreamParams<T, L> &p, unsigned char *smem_raw,
                                                unsigned &phase) {
   using C = SCfg<T, L, NS>;
@@ -234,13 +251,15 @@ __device__ __forceinline__ void syn_level_runs(const SynStreamParams<T, L> &p, u
           P ov[SP];
 #pragma unroll
           for (int j = 0; j < SP; j++) ov[j] = zero2<P>();
+          using TS = SynTaps<L, ZV>;
 #pragma unroll
           for (int q = 0; q < H; q++) {  // tap-outer: two tap pairs live at a time
             const P gl = p.g1lo[q], gh = p.g1hi[q];
+            // pair q = (g[2q+1], g[2q]): skipped when both taps are structural zeros
 #pragma unroll
             for (int j = 0; j < SP; j++) {
-              ov[j] = fma2(gl, splat2<P>(a[j + q]), ov[j]);
-              ov[j] = fma2(gh, splat2<P>(d[j + q]), ov[j]);
+              if (2 * q + 2 > TS::l0 && 2 * q < TS::l1) ov[j] = fma2(gl, splat2<P>(a[j + q]), ov[j]);
+              if (2 * q + 2 > TS::h0 && 2 * q < TS::h1) ov[j] = fma2(gh, splat2<P>(d[j + q]), ov[j]);
             }
           }
           T *vrow = (pr == 0 ? vl : vh) + (H - 1 + row1) * C::TWP + 2 * SP * seg1;
@@ -270,15 +289,16 @@ __device__ __forceinline__ void syn_level_runs(const SynStreamParams<T, L> &p, u
         P e[VC], o[VC];
 #pragma unroll
         for (int v = 0; v < VC; v++) e[v] = o[v] = zero2<P>();
+        using TS0 = SynTaps<L, ZV>;
 #pragma unroll
         for (int q = 0; q < H; q++) {
           const P el = p.e_lo[q], ol = p.o_lo[q], eh = p.e_hi[q], oh = p.o_hi[q];
 #pragma unroll
-          for (int v = 0; v < VC; v++) {
-            e[v] = fma2(el, wl[v + q], e[v]);
-            o[v] = fma2(ol, wl[v + q], o[v]);
-            e[v] = fma2(eh, wh[v + q], e[v]);
-            o[v] = fma2(oh, wh[v + q], o[v]);
+          for (int v = 0; v < VC; v++) {  // e: g[2q+1], o: g[2q]; structural zeros skipped
+            if (tap_in<TS0::l0, TS0::l1>(2 * q + 1)) e[v] = fma2(el, wl[v + q], e[v]);
+            if (tap_in<TS0::l0, TS0::l1>(2 * q)) o[v] = fma2(ol, wl[v + q], o[v]);
+            if (tap_in<TS0::h0, TS0::h1>(2 * q + 1)) e[v] = fma2(eh, wh[v + q], e[v]);
+            if (tap_in<TS0::h0, TS0::h1>(2 * q)) o[v] = fma2(oh, wh[v + q], o[v]);
           }
         }
         // fast path: every output row of the item lies in the run and the image, pair stores
@@ -328,7 +348,7 @@ __device__ __forceinline__ void syn_level_runs(const SynStreamParams<T, L> &p, u
   }
 }
 
-template <typename T, int L, int NS>
+template <typename T, int L, int NS, int ZV = 0>
 __global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 768 / SCfg<T, L>::NT : 1)
     k_synth_stream(const __grid_constant__ SynStreamParams<T, L> p) {
   using C = SCfg<T, L, NS>;
@@ -341,7 +361,7 @@ __global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 768 / SCfg<T,
   pdl_launch_dependents();
   pdl_wait();  // the previous kernel of the stream wrote our inputs
   unsigned phase = 0;
-  syn_level_runs<T, L, NS>(p, smem_raw, phase);
+  syn_level_runs<T, L, NS, ZV>(p, smem_raw, phase);
 }
 
 // The coarse head of a W chain (levels J .. j0, coarse -> fine) in one persistent cooperative
@@ -450,7 +470,7 @@ cudaError_t make_syn_params(const SynthesisArgs &a, SynStreamParams<T, L> &p, bo
   return cudaSuccess;
 }
 
-template <typename T, int L>
+template <typename T, int L, int ZV = 0>
 cudaError_t launch_synth_stream_t(const SynthesisArgs &a, cudaStream_t s) {
   using C = SCfg<T, L>;
   using C4 = SCfg<T, L, 4>;
@@ -460,15 +480,17 @@ cudaError_t launch_synth_stream_t(const SynthesisArgs &a, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   long long resident = 0;
   if (short_run) {
-    e = kernel_resident(reinterpret_cast<const void *>(k_synth_stream<T, L, 4>), C4::NT, C4::smem_bytes(), &resident);
+    e = kernel_resident(reinterpret_cast<const void *>(k_synth_stream<T, L, 4, ZV>), C4::NT, C4::smem_bytes(),
+                        &resident);
     if (e != cudaSuccess) return e;
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
-    e = launch_pdl(k_synth_stream<T, L, 4>, grid, C4::NT, C4::smem_bytes(), s, p, 's');
+    e = launch_pdl(k_synth_stream<T, L, 4, ZV>, grid, C4::NT, C4::smem_bytes(), s, p, 's');
   } else {
-    e = kernel_resident(reinterpret_cast<const void *>(k_synth_stream<T, L, 0>), C::NT, C::smem_bytes(), &resident);
+    e = kernel_resident(reinterpret_cast<const void *>(k_synth_stream<T, L, 0, ZV>), C::NT, C::smem_bytes(),
+                        &resident);
     if (e != cudaSuccess) return e;
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
-    e = launch_pdl(k_synth_stream<T, L, 0>, grid, C::NT, C::smem_bytes(), s, p, 'S');
+    e = launch_pdl(k_synth_stream<T, L, 0, ZV>, grid, C::NT, C::smem_bytes(), s, p, 'S');
   }
   g_launches++;
   if (e != cudaSuccess) return e;
@@ -477,7 +499,7 @@ cudaError_t launch_synth_stream_t(const SynthesisArgs &a, cudaStream_t s) {
 
 // A whole W chain given coarse -> fine (a[0] = level J): its short head (>= 2 levels) as one
 // cooperative k_synth_multi launch, then the long levels one launch each (only with WL_MULTI: per-level PDL launches measured faster).
-template <typename T, int L>
+template <typename T, int L, int ZV = 0>
 cudaError_t launch_syn_chain_t(const SynthesisArgs *a, int n, cudaStream_t s) {
   using C4 = SCfg<T, L, 4>;
   int nshort = 0;  // coarse levels are short first: count the leading short ones
@@ -515,7 +537,7 @@ cudaError_t launch_syn_chain_t(const SynthesisArgs *a, int n, cudaStream_t s) {
     if (e != cudaSuccess) return e;
   }
   for (int i = nmulti; i < n; i++) {
-    cudaError_t e = launch_synth_stream_t<T, L>(a[i], s);
+    cudaError_t e = launch_synth_stream_t<T, L, ZV>(a[i], s);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -527,7 +549,12 @@ cudaError_t dispatch(const SynthesisArgs &a, cudaStream_t s) {
     case 2: return launch_synth_stream_t<T, 2>(a, s);
     case 4: return launch_synth_stream_t<T, 4>(a, s);
     case 8: return launch_synth_stream_t<T, 8>(a, s);
-    case 10: return launch_synth_stream_t<T, 10>(a, s);
+    case 10:
+      switch (zero_taps_enabled() ? match_tap_range(a.lo, a.hi, 10) : 0) {
+        case 1: return launch_synth_stream_t<T, 10, 1>(a, s);
+        case 2: return launch_synth_stream_t<T, 10, 2>(a, s);
+        default: return launch_synth_stream_t<T, 10>(a, s);
+      }
     case 16: return launch_synth_stream_t<T, 16>(a, s);
   }
   return cudaErrorInvalidValue;
@@ -539,7 +566,12 @@ cudaError_t dispatch_chain(const SynthesisArgs *a, int n, cudaStream_t s) {
     case 2: return launch_syn_chain_t<T, 2>(a, n, s);
     case 4: return launch_syn_chain_t<T, 4>(a, n, s);
     case 8: return launch_syn_chain_t<T, 8>(a, n, s);
-    case 10: return launch_syn_chain_t<T, 10>(a, n, s);
+    case 10:
+      switch (zero_taps_enabled() ? match_tap_range(a[0].lo, a[0].hi, 10) : 0) {
+        case 1: return launch_syn_chain_t<T, 10, 1>(a, n, s);
+        case 2: return launch_syn_chain_t<T, 10, 2>(a, n, s);
+        default: return launch_syn_chain_t<T, 10>(a, n, s);
+      }
     case 16: return launch_syn_chain_t<T, 16>(a, n, s);
   }
   return cudaErrorInvalidValue;

@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -69,6 +70,30 @@ bool encode_tmap_3d(void *map, int elem_bytes, const void *base, uint64_t d0, ui
 bool tma_enabled() {
   static const bool v = getenv("WL_NO_TMA") == nullptr;
   return v;
+}
+
+bool zero_taps_enabled() {
+  static const bool v = getenv("WL_ALL_TAPS") == nullptr;
+  return v;
+}
+
+int match_tap_range(const double *lo, const double *hi, int L) {
+  if (L != 10) return 0;
+  auto range = [&](const double *f, int &a, int &b) {
+    a = L;
+    b = 0;
+    for (int j = 0; j < L; j++)
+      if (f[j] != 0.0) {
+        a = std::min(a, j);
+        b = std::max(b, j + 1);
+      }
+  };
+  int l0, l1, h0, h1;
+  range(lo, l0, l1);
+  range(hi, h0, h1);
+  if (l0 == 2 && l1 == 9 && h0 == 0 && h1 == 9) return 1;
+  if (l0 == 1 && l1 == 10 && h0 == 1 && h1 == 8) return 2;
+  return 0;
 }
 
 bool multi_enabled() {

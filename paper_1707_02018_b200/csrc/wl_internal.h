@@ -151,6 +151,12 @@ int short_run_max(int dflt);
 
 // TMA loads unless WL_NO_TMA is set (debugging / A-B switch); read once per process
 bool tma_enabled();
+// Structural-zero tap variants: 1 if (lo, hi) are the CDF 9/7 dual filters of the
+// L = 10 frame (d_lo nonzero on [2, 9), d_hi on [0, 9)), 2 if the analysis filters (a_lo on
+// [1, 10), a_hi on [1, 8)), 0 otherwise.  The kernels then skip the zero taps at compile time.
+int match_tap_range(const double *lo, const double *hi, int L);
+// zero-tap skipping unless WL_ALL_TAPS is set (A-B switch)
+bool zero_taps_enabled();
 // multi-level persistent launches for the coarse tails only when WL_MULTI is set (A-B switch)
 bool multi_enabled();
 
