@@ -89,7 +89,9 @@ struct ACfg {
   // 4 (cfg4 W* -3.6 %), the shorter filters with 8
   static constexpr int VC = (F32 && !SMALL) ? (L >= 16 ? 4 : WL_ANA_VC) : 4;
   static constexpr int SHIFT = ((2 - L) % VEC + VEC) % VEC;  // box column of input column 2q0+2-L
-  static constexpr int UW = round_up_c(SHIFT + 2 * TQ + L - 2, VEC);  // input box width
+  // input box width, padded so that a row is 4 mod 8 words: the B-stage 16-byte window loads of 8
+  // consecutive rows then fall in 8 distinct 4-bank groups (row-fastest items, no bank conflicts)
+  static constexpr int UW = bank_pad<T>(round_up_c(SHIFT + 2 * TQ + L - 2, VEC));
   static constexpr int UP = UW;                          // dense TMA box rows
   static constexpr int NV = UW / VEC;
   static constexpr int NWB = round_up_c(SHIFT + 2 * V + L - 2, VEC);  // B window
@@ -201,9 +203,9 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
     const double t = *p.tdev, t_new = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
     mom = T((t - 1.0) / t_new);
   }
-  // B item: segment fastest; C item: column pair fastest, then set (lo / hi), then group
+  // B item: input row fastest; C item: column pair fastest, then set (lo / hi), then group
   const bool actB = tid < C::ITEMS_B;
-  const int segB = tid % C::SEGB, rowB = tid / C::SEGB;
+  const int rowB = tid % C::GI, segB = tid / C::GI;  // row fastest: a warp's loads hit distinct banks
   const bool actC = tid < C::ITEMS_C;
   const int mC = tid % (TQ / 2), setC = (tid / (TQ / 2)) & 1, grpC = tid / TQ;
 

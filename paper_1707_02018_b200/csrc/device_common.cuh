@@ -75,6 +75,16 @@ constexpr int conflict_free_pitch(int n) {
 
 constexpr int round_up_c(int v, int a) { return (v + a - 1) / a * a; }
 
+// Smallest row length (elements, a multiple of the 16-byte vector) >= n whose size in 4-byte words
+// is 4 mod 8: 16-byte accesses of 8 consecutive rows at one column hit 8 distinct 4-bank groups.
+template <typename T>
+constexpr int bank_pad(int n) {
+  const int vec = 16 / (int)sizeof(T);
+  int p = round_up_c(n, vec);
+  while (((p * (int)sizeof(T) / 4) % 8) != 4) p += vec;
+  return p;
+}
+
 // Packed pair arithmetic: float2 maps to FFMA2 / FADD2 (sm_100a), double2 to two FMAs.
 template <typename T>
 struct Pair;

@@ -59,7 +59,7 @@ struct SCfg {
 #endif
   static constexpr int SP = sizeof(T) == 4 ? WL_SYN_SP : 8;   // output column pairs per S1 item
   static constexpr int VC = sizeof(T) == 4 ? WL_SYN_VC : 4;   // s-values (output row pairs) per S0 item
-  static constexpr int KCW = round_up_c(TW / 2 + H - 1, VEC);  // coefficient columns loaded
+  static constexpr int KCW = bank_pad<T>(TW / 2 + H - 1);  // coefficient columns loaded (rows 4 mod 8 words)
   static constexpr int KCP = KCW;                        // dense TMA box rows
   static constexpr int NWC = round_up_c(SP + H - 1, VEC);  // S1 window per subband
   static constexpr int NSEG = TW / (2 * SP);
@@ -132,9 +132,11 @@ __device__ __forceinline__ void syn_level_runs(const SynStreamParams<T, L> &p, u
   T *vh = vl + C::HR * C::TWP;                           // [HR][TWP] VH history
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + C::OFF_BAR);
   const int tid = threadIdx.x;
-  // S1 item: segment fastest; S0 item: column pair fastest
+  // S1 item: coefficient row fastest; S0 item: column pair fastest
   const bool act1 = tid < C::ITEMS1;
-  const int seg1 = tid % C::NSEG, row1 = tid / C::NSEG;
+  // row fastest: the 16-byte V-history stores of 8 consecutive rows (pitch 4 mod 8 words) and the
+  // coefficient window loads (box rows 4 mod 8 words) hit 8 distinct 4-bank groups
+  const int row1 = tid % G, seg1 = tid / G;
   const bool act0 = tid < C::ITEMS0;
   const int m0c = tid % (C::TW / 2), grp0 = tid / (C::TW / 2);
 
