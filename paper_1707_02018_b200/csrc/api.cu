@@ -270,14 +270,16 @@ wl_status run_synthesis(const wl_plan *p, int64_t batch, const void *x, void *im
     if (sym) {
       // synthesize onto [-L', n+L') per axis, then fold: E_sym^dagger (W of EDAG) or
       // E_sym^T ((W-dagger)* under symmetric BC)
-      int64_t ep = round_up(n1 + 2 * Lp, 16 / p->es);
+      // U columns start one position earlier, at t = -L (even): output column pairs then sit at
+      // even U indices and the synthesis stores them as aligned pairs (the extra column is 0)
+      int64_t ep = round_up(n1 + 2 * Lp + 1, 16 / p->es);
       a.out = ws + L.e;
       a.out_pitch = ep;
       a.out_bstride = p->edag_elems;
       a.N0 = (int)(n0 + 2 * Lp);
-      a.N1 = (int)(n1 + 2 * Lp);
+      a.N1 = (int)(n1 + 2 * Lp + 1);
       a.o0 = -Lp;
-      a.o1 = -Lp;
+      a.o1 = -Lp - 1;
       cudaError_t e = launch_synthesis(p->dtype, a, s);
       if (e != cudaSuccess) return cuda_fail(e, "synthesis level launch");
       FoldArgs f;
@@ -292,6 +294,7 @@ wl_status run_synthesis(const wl_plan *p, int64_t batch, const void *x, void *im
       f.Lp = Lp;
       f.weighted = transpose_of_analysis ? 0 : 1;
       f.batch = (int)batch;
+      f.col_off = 1;
       e = launch_fold(p->dtype, f, s);
       if (e != cudaSuccess) return cuda_fail(e, "fold launch");
     } else {
@@ -414,7 +417,7 @@ wl_status wl_plan_create(wl_plan **out, int64_t h, int64_t w, int levels, wl_fil
   }
   if (bc == WL_BC_SYMMETRIC_EDAG || bc == WL_BC_SYMMETRIC)  // extended synthesis buffer (W of EDAG, (W-dagger)*)
     for (int j = 1; j <= levels; j++)
-      p->edag_elems = std::max(p->edag_elems, (p->n0[j - 1] + 2 * (L - 1)) * round_up(p->n1[j - 1] + 2 * (L - 1), align));
+      p->edag_elems = std::max(p->edag_elems, (p->n0[j - 1] + 2 * (L - 1)) * round_up(p->n1[j - 1] + 2 * (L - 1) + 1, align));
   *out = p;
   return ok();
 }

@@ -21,7 +21,8 @@ namespace {
 template <typename T>
 __global__ void __launch_bounds__(256) k_fold_sym_pinv(const T *__restrict__ U, long long upitch, long long ubs,
                                                        T *__restrict__ y, long long ypitch, long long ybs, int n0,
-                                                       int n1, int Lp, int weighted, int vec, long long nrows) {
+                                                       int n1, int Lp, int weighted, int vec, long long nrows,
+                                                       int coff) {
   const int p0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (p0 >= n1) return;
   // (image, row) pairs flattened over gridDim.y with a stride loop: any batch and height
@@ -31,7 +32,7 @@ __global__ void __launch_bounds__(256) k_fold_sym_pinv(const T *__restrict__ U, 
   T *yo = y + (long long)b * ybs + (long long)i * ypitch;
   const bool row_in = i >= Lp && i < n0 - Lp;
   if (row_in && p0 >= Lp && p0 + 4 <= n1 - Lp) {
-    const T *ur = u + (long long)(i + Lp) * upitch + (p0 + Lp);
+    const T *ur = u + (long long)(i + Lp) * upitch + (p0 + Lp + coff);
     const T v[4] = {ur[0], ur[1], ur[2], ur[3]};
     if (vec) {  // 16-byte aligned output rows (fp32) / 2 x 16 bytes (fp64)
       using Vt = typename Vec16<T>::type;
@@ -57,7 +58,7 @@ __global__ void __launch_bounds__(256) k_fold_sym_pinv(const T *__restrict__ U, 
     if (pcol >= n1 - Lp) t1s[c1++] = 2 * n1 - 1 - pcol;
     T acc = T(0);
     for (int a = 0; a < c0; a++)
-      for (int c = 0; c < c1; c++) acc += u[(long long)(t0s[a] + Lp) * upitch + (t1s[c] + Lp)];
+      for (int c = 0; c < c1; c++) acc += u[(long long)(t0s[a] + Lp) * upitch + (t1s[c] + Lp + coff)];
     yo[pcol] = weighted ? acc / T(c0 * c1) : acc;
   }
   }
@@ -73,11 +74,11 @@ cudaError_t launch_fold(int dtype, const FoldArgs &a, cudaStream_t s) {
   if (dtype == WL_F64)
     k_fold_sym_pinv<double><<<grid, 256, 0, s>>>(static_cast<const double *>(a.in), a.in_pitch, a.in_bstride,
                                                  static_cast<double *>(a.out), a.out_pitch, a.out_bstride, a.n0,
-                                                 a.n1, a.Lp, a.weighted, vec, nrows);
+                                                 a.n1, a.Lp, a.weighted, vec, nrows, a.col_off);
   else
     k_fold_sym_pinv<float><<<grid, 256, 0, s>>>(static_cast<const float *>(a.in), a.in_pitch, a.in_bstride,
                                                static_cast<float *>(a.out), a.out_pitch, a.out_bstride, a.n0,
-                                               a.n1, a.Lp, a.weighted, vec, nrows);
+                                               a.n1, a.Lp, a.weighted, vec, nrows, a.col_off);
   g_launches++;
   return cudaGetLastError();
 }

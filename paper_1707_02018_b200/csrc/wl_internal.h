@@ -65,6 +65,7 @@ struct FoldArgs {  // y = diag(1/c) E_sym^T U per axis (weighted: W of SYMMETRIC
   int n0, n1, Lp;
   int weighted;                  // 1: E_sym^dagger = diag(1/c) E_sym^T; 0: E_sym^T ((W-dagger)*)
   int batch;
+  int col_off = 0;               // U column of extended position t is t + Lp + col_off
 };
 
 struct BlurArgs {
