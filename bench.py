@@ -377,6 +377,17 @@ def run_wl(args):
              "traffic": traffic_from_profiles("wstar_cfg4_chain")}
     del y4, x4, ws4
 
+    # ---- the same gradient with the paper-literal symmetric adjoint (bc = symmetric_edag, reading R1
+    # "P": W*_P = W~dagger_zpd (E_sym^dagger)*, Eq. (4)), the variant the paper's Fig. 2-3 runs
+    plan_e = wl.Plan(c.h, c.w, c.levels, c.filt, "symmetric_edag", c.dtype)
+    xe = plan_e.from_packed(plan.to_packed(x))
+    ge = torch.empty_like(xe)
+    wse = plan_e._ws(wl.OP_GRAD, B, blur=blur)
+    de = time_dist(torch, wl.Graph(lambda: wl.grad(plan_e, blur, xe, b, out=ge, ws=wse)).replay, max(args.steps, 20), flush)
+    grad_edag = {"ms": de["median_ms"], "GB/s": grad_bytes(B, N, plan_e.p_valid, es) / (de["median_ms"] * 1e-3) / 1e9,
+                 "cold": de, "config": "cfg5 with bc=symmetric_edag", "launch": "cuda_graph"}
+    del xe, ge, wse
+
     # ---- one FISTA iteration at cfg5 (grad f(y) + fused prox/momentum update)
     xf, yf = torch.zeros_like(x), x.clone()
     wsf = plan._ws(wl.OP_FISTA, B, blur=blur)
@@ -481,7 +492,7 @@ def run_wl(args):
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(), "step_launch": "eager" if graph is None else "cuda_graph",
                 "ms_per_step_eager": ms_eager, "step_distribution": step_dist, "l2_bytes": l2_bytes, "grad_evals_per_s": ws / (ms * 1e-3), "images_per_s": ws * B / (ms * 1e-3),
-                "grad_frac_of_hbm_roofline": value / ws / hbm_peak, "wstar_cfg4": wstar, "fista_cfg5": fista, "bce": bce, "operators_by_config": per_cfg, "kernels": kernels}
+                "grad_frac_of_hbm_roofline": value / ws / hbm_peak, "wstar_cfg4": wstar, "grad_cfg5_symmetric_edag": grad_edag, "fista_cfg5": fista, "bce": bce, "operators_by_config": per_cfg, "kernels": kernels}
         print(json.dumps(line))
     if ws > 1:
         import torch.distributed as dist
