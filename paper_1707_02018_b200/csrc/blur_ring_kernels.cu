@@ -39,6 +39,20 @@ namespace {
 
 constexpr int kRing = 15;  // register-ring slots: the vertical window of the largest PSF taken here
 
+#ifdef WL_RING_PROFILE  // debug builds only: per-run start / end times and SM id (tools/ringprof.py)
+__device__ unsigned long long g_ring_prof[8192][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+#endif
+
 template <int HW, bool RESID>
 struct RingCfg {
   static_assert(2 * HW + 1 <= kRing, "ring too short for this PSF");
@@ -194,6 +208,9 @@ __global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_co
     int col, r0, r1;
     p.runs.get(run, col, r0, r1);
     if (r0 >= r1) continue;  // (uniform) empty trailing band
+#ifdef WL_RING_PROFILE
+    const unsigned long long t_start = gtimer();
+#endif
     const int img = col / p.nstrips, strip = col - img * p.nstrips;
     const int c0 = strip * C::T;
     const int col1 = RESID ? c0 - HW : c0;  // image column of stage-1 pair 0
@@ -280,9 +297,12 @@ __global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_co
         mbar_wait(full + st, (g / S) & 1);
         float *ust = ubase + st * 2 * C::UREG;
         if (uedge) {
-          if (ufix_t >= 0) {
+          if (ufix_t >= 0) {  // all G loads first, then the stores: one shared-memory latency
+            float v[G];
 #pragma unroll
-            for (int r = 0; r < G; r++) ust[r * C::UBOX + ufix_t] = ust[r * C::UBOX + ufix_s];
+            for (int r = 0; r < G; r++) v[r] = ust[r * C::UBOX + ufix_s];
+#pragma unroll
+            for (int r = 0; r < G; r++) ust[r * C::UBOX + ufix_t] = v[r];
           }
           __syncwarp();
         }
@@ -331,8 +351,11 @@ __global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_co
         if (RESID && (k + 1) * G > 2 * HW) {
           if (redge) {
             if (rfix_t >= 0) {
+              float v[G];
 #pragma unroll
-              for (int r = 0; r < G; r++) rw[r * C::NC + rfix_t] = rw[r * C::NC + rfix_s];
+              for (int r = 0; r < G; r++) v[r] = rw[r * C::NC + rfix_s];
+#pragma unroll
+              for (int r = 0; r < G; r++) rw[r * C::NC + rfix_t] = v[r];
             }
             __syncwarp();
           }
@@ -363,6 +386,15 @@ __global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_co
       }
     }
     gbase += n_groups;
+#ifdef WL_RING_PROFILE
+    __syncthreads();
+    if (tid == 0 && run < 8192) {
+      g_ring_prof[run][0] = t_start;
+      g_ring_prof[run][1] = gtimer();
+      g_ring_prof[run][2] = smid();
+      g_ring_prof[run][3] = ((unsigned long long)col << 32) | (unsigned)(r1 - r0);
+    }
+#endif
     if (RESID && p.f) {
       for (int o = 16; o > 0; o >>= 1) fsum += __shfl_xor_sync(0xffffffffu, fsum, o);
       if ((tid & 31) == 0) atomicAdd(p.f + img, 0.5 * fsum);
@@ -417,6 +449,12 @@ bool ring_disabled() {
 }
 
 }  // namespace
+
+#ifdef WL_RING_PROFILE
+extern "C" __attribute__((visibility("default"))) int wl_debug_ring_prof(void *host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_ring_prof, sizeof(unsigned long long) * 4 * (size_t)n);
+}
+#endif
 
 bool launch_blur_ring(int dtype, const BlurArgs &a, bool residual, cudaStream_t s, cudaError_t *err) {
   if (dtype != WL_F32 || ring_disabled() || !tma_enabled()) return false;
