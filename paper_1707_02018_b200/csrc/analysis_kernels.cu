@@ -55,6 +55,9 @@ __device__ __forceinline__ int ext_src(int t, int n, int ext, int Lp, T &w) {
   return s;
 }
 
+#ifndef WL_ANA_NS
+#define WL_ANA_NS 2  // A/B on B200: 3 or 4 stages did not beat 2
+#endif
 template <typename T, int L, int NS_ = 0, bool FU_ = false>
 struct ACfg {
   using P = typename Pair<T>::t;
@@ -89,9 +92,23 @@ struct ACfg {
   // 4 (cfg4 W* -3.6 %), the shorter filters with 8
   static constexpr int VC = (F32 && !SMALL) ? (L >= 16 ? 4 : WL_ANA_VC) : 4;
   static constexpr int SHIFT = ((2 - L) % VEC + VEC) % VEC;  // box column of input column 2q0+2-L
-  // input box width, padded so that a row is 4 mod 8 words: the B-stage 16-byte window loads of 8
-  // consecutive rows then fall in 8 distinct 4-bank groups (row-fastest items, no bank conflicts)
-  static constexpr int UW = bank_pad<T>(round_up_c(SHIFT + 2 * TQ + L - 2, VEC));
+  // input box width.  Padded so that a row is 4 mod 8 words (the B-stage 16-byte window loads of 8
+  // consecutive rows then fall in 8 distinct 4-bank groups: row-fastest items, no bank conflicts)
+  // unless the padding would cost a resident CTA per SM (B200: CDF 9/7 keeps 4 CTAs with dense
+  // rows and 2-way conflicts, measured 1 % faster; db8 has 3 CTAs either way and pads)
+  static constexpr int UW0 = round_up_c(SHIFT + 2 * TQ + L - 2, VEC);
+  static constexpr int UWP = bank_pad<T>(UW0);
+  static constexpr int HR_ = L - 2 + 2 * G;
+  static constexpr int NS0 = NS_ > 0 ? NS_ : WL_ANA_NS;
+  static constexpr int ctas_for(int uw) {
+    return (228 * 1024) / (round_up_c(NS0 * 2 * G * uw * (int)sizeof(T), 128) +
+                           2 * HR_ * conflict_free_pitch<T>(TQ) * (int)sizeof(T) + 16 + 1024);
+  }
+#ifdef WL_ANA_NOPAD  // A/B: dense box rows always
+  static constexpr int UW = UW0;
+#else
+  static constexpr int UW = ctas_for(UWP) >= ctas_for(UW0) ? UWP : UW0;
+#endif
   static constexpr int UP = UW;                          // dense TMA box rows
   static constexpr int NV = UW / VEC;
   static constexpr int NWB = round_up_c(SHIFT + 2 * V + L - 2, VEC);  // B window
@@ -103,9 +120,6 @@ struct ACfg {
   static constexpr int ITEMS_B = SEGB * GI;
   static constexpr int ITEMS_C = 2 * (TQ / 2) * (G / VC);
   static constexpr int NT = round_up_c(std::max(ITEMS_B, ITEMS_C), 32);
-#ifndef WL_ANA_NS
-#define WL_ANA_NS 2  // A/B on B200: 3 or 4 stages did not beat 2
-#endif
   // input stages (prefetch depth NS-1); short runs (coarse levels) use 4 so every block of the
   // run is in flight at once instead of one TMA round trip per block
   static constexpr int NS = NS_ > 0 ? NS_ : WL_ANA_NS;
