@@ -93,7 +93,7 @@ struct RingParams {
   const float *b;
   float *out;
   double *f;  // residual only (nullable)
-  int h, w, nstrips;
+  int h, w, nstrips, batch;
   RunMap runs;
   float cv[HW + 1];               // c[d] = k[HW - d] for d <= HW (symmetric PSF: c[2HW - d] = c[d])
   float2 ce[HW + 1], co[HW + 1];  // (c[2m], c[2m+1]) and (c[2m-1], c[2m]), out-of-range taps 0
@@ -211,7 +211,20 @@ __global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_co
 #ifdef WL_RING_PROFILE
     const unsigned long long t_start = gtimer();
 #endif
-    const int img = col / p.nstrips, strip = col - img * p.nstrips;
+    // column order: the edge strips of every image first (they cost more per row: mirror fixes),
+    // so RunMap's first columns -- the ones cut into one band more -- carry them (SM balance)
+    int img, strip;
+    if (p.nstrips >= 3 && col < 2 * p.batch) {
+      img = col >> 1;
+      strip = (col & 1) ? p.nstrips - 1 : 0;
+    } else if (p.nstrips >= 3) {
+      const int k = col - 2 * p.batch;
+      img = k / (p.nstrips - 2);
+      strip = 1 + k - img * (p.nstrips - 2);
+    } else {
+      img = col / p.nstrips;
+      strip = col - img * p.nstrips;
+    }
     const int c0 = strip * C::T;
     const int col1 = RESID ? c0 - HW : c0;  // image column of stage-1 pair 0
     const int ustart = floor4(col1 - HW);    // u box 0 origin (16-byte aligned)
@@ -414,6 +427,7 @@ cudaError_t launch_ring(const BlurArgs &a, cudaStream_t s) {
   p.h = (int)a.h;
   p.w = (int)a.w;
   p.nstrips = (int)((a.w + C::T - 1) / C::T);
+  p.batch = a.batch;
   const uint64_t rs = (uint64_t)p.w * 4, is = rs * (uint64_t)p.h;
   if (!encode_tmap_3d(&p.tmap_u, 4, a.in, p.w, p.h, a.batch, rs, is, C::UBOX, C::G)) return cudaErrorNotSupported;
   if (RESID && !encode_tmap_3d(&p.tmap_b, 4, a.b, p.w, p.h, a.batch, rs, is, C::BBOX, C::G))
