@@ -96,43 +96,32 @@ struct RingParams {
   int h, w, nstrips, batch;
   RunMap runs;
   float cv[HW + 1];               // c[d] = k[HW - d] for d <= HW (symmetric PSF: c[2HW - d] = c[d])
-  float2 ce[HW + 1], co[HW + 1];  // (c[2m], c[2m+1]) and (c[2m-1], c[2m]), out-of-range taps 0
+  float2 cs[2 * HW + 1];          // (c[d], c[d]): FFMA2 taps of the aligned window pairs
 };
 
 __device__ __forceinline__ int ocol_of(int c0, int tid) { return c0 + 2 * tid; }
 __device__ __forceinline__ int floor4(int v) { return v >= 0 ? (v & ~3) : -(((-v) + 3) & ~3); }
 
 // Pair (out[s0], out[s0+1]) of a 2HW+1-tap correlation over the window w (s0 = S0):
-// out[s] = sum_d c[d] w[s + d].  Even s: (even, odd) tap pairs; odd s: (odd, even).
+// out[s] = sum_d c[d] w[s + d].  Taps d whose sample pair (w[s0+d], w[s0+d+1]) is an aligned
+// register pair of the window (s0 + d even) take one FFMA2 with the splat tap (c[d], c[d]); the
+// others are two scalar FFMAs into a second accumulator pair (their samples straddle two pairs).
+// 2HW+1 lane-FMAs per output and no cross-lane reduction: the FMA pipe does the minimum work.
 template <int HW, int S0>
 __device__ __forceinline__ float2 hpair(const float *w, const RingParams<HW> &p) {
-#ifndef WL_RING_HCHAINS
-#define WL_RING_HCHAINS 2
-#endif
-  // WL_RING_HCHAINS independent accumulator chains per output (ILP for the FMA pipe)
-  constexpr int NCH = WL_RING_HCHAINS;
-  float2 a[NCH], b[NCH];
+  float2 a = make_float2(0.f, 0.f), b = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int c = 0; c < NCH; c++) a[c] = b[c] = make_float2(0.f, 0.f);
-#pragma unroll
-  for (int m = 0; m <= HW; m++) {
-    if (S0 == 0) {
-      const float2 x = make_float2(w[2 * m], w[2 * m + 1]);
-      a[m % NCH] = fma2(p.ce[m], x, a[m % NCH]);   // out[0]: w[2m] c[2m] + w[2m+1] c[2m+1]
-      b[m % NCH] = fma2(p.co[m], x, b[m % NCH]);   // out[1]: w[2m] c[2m-1] + w[2m+1] c[2m]
+  for (int d = 0; d <= 2 * HW; d++) {
+    const int s = S0 + d;
+    if (s % 2 == 0) {
+      a = fma2(p.cs[d], make_float2(w[s], w[s + 1]), a);
     } else {
-      const float2 x = make_float2(w[2 * m], w[2 * m + 1]);
-      const float2 y = make_float2(w[2 * m + 2], w[2 * m + 3]);
-      a[m % NCH] = fma2(p.co[m], x, a[m % NCH]);   // out[1] (window position 1)
-      b[m % NCH] = fma2(p.ce[m], y, b[m % NCH]);   // out[2]
+      const float c = p.cs[d].x;
+      b.x = fmaf(c, w[s], b.x);
+      b.y = fmaf(c, w[s + 1], b.y);
     }
   }
-#pragma unroll
-  for (int c = 1; c < NCH; c++) {
-    a[0] = add2(a[0], a[c]);
-    b[0] = add2(b[0], b[c]);
-  }
-  return make_float2(a[0].x + a[0].y, b[0].x + b[0].y);
+  return add2(a, b);
 }
 
 // Row-wise loads of one operand box of a group that reaches past the top or bottom of the image:
@@ -164,14 +153,14 @@ __device__ __forceinline__ void st_pair_if(float *ptr, float2 v, bool pred) {
 template <int HW>
 __device__ __forceinline__ float2 vring(const float2 (&ring)[kRing], int nw, const RingParams<HW> &p, float2 init) {
   const int lo = nw - 2 * HW + kRing;
-  float2 a = fma2(splat2<float2>(p.cv[HW]), ring[(lo + HW) % kRing], init), b = make_float2(0.f, 0.f);
+  // one accumulator chain (HW + 1 FFMA2; the HW pre-adds are independent): no final add
+  float2 a = fma2(splat2<float2>(p.cv[HW]), ring[(lo + HW) % kRing], init);
 #pragma unroll
   for (int d = 0; d < HW; d++) {
     const float2 sp = add2(ring[(lo + d) % kRing], ring[(lo + 2 * HW - d) % kRing]);
-    if (d % 2 == 0) b = fma2(splat2<float2>(p.cv[d]), sp, b);
-    else a = fma2(splat2<float2>(p.cv[d]), sp, a);
+    a = fma2(splat2<float2>(p.cv[d]), sp, a);
   }
-  return add2(a, b);
+  return a;
 }
 
 #ifndef WL_RING_MINB
@@ -212,7 +201,10 @@ __global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_co
     const unsigned long long t_start = gtimer();
 #endif
     // column order: the edge strips of every image first (they cost more per row: mirror fixes),
-    // so RunMap's first columns -- the ones cut into one band more -- carry them (SM balance)
+    // so RunMap's first columns -- the ones cut into one band more -- carry them (SM balance).
+    // (A split into equal-cost parts that continue across columns measured slower: the SMs'
+    // speeds differ by up to 20 % on identical parts, and the neighbouring strips' halo columns
+    // no longer meet in L2.)
     int img, strip;
     if (p.nstrips >= 3 && col < 2 * p.batch) {
       img = col >> 1;
@@ -325,6 +317,11 @@ __global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_co
         float2 fa = make_float2(0.f, 0.f);
         // output row of step 0 of this group (stage 1 for R, stage 2 for the residual)
         float *orow = obase + (long long)((RESID ? brow0 : urow0) + k * G - HW) * w;
+        // rows r of this group with a stored output: olo <= r < ohi (the first 2HW (R) / 4HW
+        // (residual) steps of a run only prime the rings); f counts rows flo <= r < fhi
+        const int olo = (RESID ? 4 * HW : 2 * HW) - k * G;
+        const int ohi = act ? r1 + HW - (RESID ? brow0 : urow0) - k * G : 0;
+        const int flo = r0 - brow0 - k * G, fhi = r1 - brow0 - k * G;
         // ---------------- stage 1: h1 = R_h u -> ring1; r = R_v h1 - b (residual) or out = R_v h1
         // (the window of step r + 1 is loaded before step r computes: WL_RING_PF)
         float2 wb[2][NWIN / 2];
@@ -333,7 +330,6 @@ __global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_co
 #pragma unroll
         for (int r = 0; r < G; r++) {
           const int slot = gg * G + r;  // == step % kRing (kb G is a multiple of kRing)
-          const int i = k * G + r;
           if (r + 1 < G) {
             const float2 *src = reinterpret_cast<const float2 *>(ub + (r + 1) * C::UBOX);
 #pragma unroll
@@ -350,11 +346,11 @@ __global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_co
             const float *bp = bb + r * C::BBOX;
             const float2 rv = vring<HW>(ring1, slot, p, make_float2(-bp[0], -bp[1]));
             *reinterpret_cast<float2 *>(rw + r * C::NC + 2 * tid) = rv;
-            const int yr = brow0 + i;
-            if (yr >= r0 && yr < r1) fa = fma2(rv, rv, fa);
+            if (r >= flo && r < fhi) fa = fma2(rv, rv, fa);
           } else {
             const float2 o = vring<HW>(ring1, slot, p, make_float2(0.f, 0.f));
-            st_pair_if(orow + r * w, o, act && i >= 2 * HW && urow0 + i - HW < r1);
+            st_pair_if(orow, o, r >= olo && r < ohi);
+            orow += w;
           }
         }
         if (RESID) fsum += (double)fa.x * mx + (double)fa.y * my;
@@ -380,7 +376,6 @@ __global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_co
 #pragma unroll
           for (int r = 0; r < G; r++) {
             const int slot = gg * G + r;
-            const int i = k * G + r;
             if (r + 1 < G) {
 #pragma unroll
               for (int j = 0; j < NWIN / 2; j++) vb[(r + 1) & 1][j] = rsrc[(r + 1) * (C::NC / 2) + j];
@@ -393,7 +388,8 @@ __global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_co
             }
             ring2[slot] = hpair<HW, 0>(win, p);
             const float2 o = vring<HW>(ring2, slot, p, make_float2(0.f, 0.f));
-            st_pair_if(orow + r * w, o, act && i >= 4 * HW && brow0 + i - HW < r1);
+            st_pair_if(orow, o, r >= olo && r < ohi);
+            orow += w;
           }
         }
       }
@@ -434,12 +430,8 @@ cudaError_t launch_ring(const BlurArgs &a, cudaStream_t s) {
     return cudaErrorNotSupported;
   double c[2 * HW + 1];
   for (int d = 0; d <= 2 * HW; d++) c[d] = a.taps[2 * HW - d];
-  auto cd = [&](int d) { return (d >= 0 && d <= 2 * HW) ? c[d] : 0.0; };
   for (int d = 0; d <= HW; d++) p.cv[d] = (float)c[d];
-  for (int m = 0; m <= HW; m++) {
-    p.ce[m] = make_float2((float)cd(2 * m), (float)cd(2 * m + 1));
-    p.co[m] = make_float2((float)cd(2 * m - 1), (float)cd(2 * m));
-  }
+  for (int d = 0; d <= 2 * HW; d++) p.cs[d] = make_float2((float)c[d], (float)c[d]);
   auto kern = k_blur_ring<HW, RESID>;
   long long resident = 0;
   cudaError_t e = kernel_resident(reinterpret_cast<const void *>(kern), C::NT, C::SMEM, &resident);
