@@ -223,10 +223,8 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
   const bool actC = tid < C::ITEMS_C;
   const int mC = tid % (TQ / 2), setC = (tid / (TQ / 2)) & 1, grpC = tid / TQ;
 
-  const int nruns = p.runs.nruns();
-  for (int run = blockIdx.x; run < nruns; run += gridDim.x) {
-    int col, kr0, kr1;
-    p.runs.get(run, col, kr0, kr1);
+  int col, kr0, kr1;
+  for (RunIter itr(p.runs); itr.next(col, kr0, kr1);) {
     if (kr0 >= kr1) continue;  // (uniform) empty trailing band
     const int img = col / p.nstrips, strip = col - img * p.nstrips;
     const int q0 = strip * TQ;
@@ -588,8 +586,9 @@ cudaError_t make_ana_params(const AnalysisArgs &a, AnaStreamParams<T, L> &p, boo
     e = kernel_resident(reinterpret_cast<const void *>(k_ana_stream<T, L, FU, 0>), C::NT, C::smem_bytes(FU),
                         &resident);
     if (e != cudaSuccess) return e;
-    p.runs = RunMap::make((long long)a.batch * p.nstrips, a.m0, resident, std::max(1, C::G * WL_ANA_MINROWS / 2), 1);
-    const int band = (a.m0 + p.runs.nb_lo - 1) / p.runs.nb_lo;
+    p.runs = RunMap::make((long long)a.batch * p.nstrips, a.m0, resident, std::max(1, C::G * WL_ANA_MINROWS / 2), 1,
+                          balanced_runs());
+    const int band = p.runs.mean_rows();
     short_run = (band + C::G - 1) / C::G <= short_run_max(3);
   }
   if (short_run) {
@@ -598,7 +597,8 @@ cudaError_t make_ana_params(const AnalysisArgs &a, AnaStreamParams<T, L> &p, boo
                           &resident4);
       if (e != cudaSuccess) return e;
     }
-    p.runs = RunMap::make((long long)a.batch * p.nstrips, a.m0, resident4, std::max(1, C4::G * WL_ANA_MINROWS / 2), 1);
+    p.runs = RunMap::make((long long)a.batch * p.nstrips, a.m0, resident4, std::max(1, C4::G * WL_ANA_MINROWS / 2), 1,
+                          balanced_runs());
     encode(C4::UW, C4::GI);
   } else {
     encode(C::UW, C::GI);

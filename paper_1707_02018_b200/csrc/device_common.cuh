@@ -181,16 +181,23 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned b
 namespace wl {
 
 // Work decomposition of the streaming kernels: `ncols` columns ((image, strip) pairs, image
-// major) of `span` rows each are cut into bands, one run per band.  The first `extra`
-// columns get nb_lo + 1 bands, the rest nb_lo, so the total number of runs can equal the
-// number of resident CTAs exactly (no tail wave) while neighbouring strips keep the same
-// band boundaries (their halo columns are then streamed through L2 at the same time).
+// major) of `span` rows, handed out as runs, one per resident CTA when the columns allow it.
+//  * banded (bal = 0): each column is cut into bands; the first `extra` columns get nb_lo + 1
+//    bands, the rest nb_lo, so the number of runs equals the resident CTAs while neighbouring
+//    strips keep the same band boundaries (their halo columns stream through L2 together);
+//  * balanced (bal = 1): the columns are laid end to end and cut into `nparts` runs of equal
+//    row count (rounded to `align`); a run may continue from the bottom of one column into the
+//    top of the next (each piece is a segment with its own priming).  With 132 columns on 444
+//    CTAs the banded split leaves bands of 513 and 684 rows; the balanced one gives every CTA
+//    the same work -- and measured far slower on B200 (cfg5 W* level 1 170 vs 108 us): strips
+//    that stream different rows at the same time lose DRAM page locality.  A/B only.
+// Iterate a CTA's segments with:  for (RunIter it(map); it.next(col, r0, r1);) { ... }
 struct RunMap {
-  int ncols, nb_lo, extra, span, align;
+  int ncols, nb_lo, extra, span, align, bal, nparts;
 
-  __host__ __device__ int nruns() const { return extra * (nb_lo + 1) + (ncols - extra) * nb_lo; }
+  __host__ __device__ int nruns() const { return bal ? nparts : extra * (nb_lo + 1) + (ncols - extra) * nb_lo; }
 
-  // run -> (column, first row, end row) with rows in [0, span)
+  // banded: run -> (column, first row, end row) with rows in [0, span)
   __device__ __forceinline__ void get(int run, int &col, int &r0, int &r1) const {
     int band, nb;
     const int big = extra * (nb_lo + 1);
@@ -209,14 +216,37 @@ struct RunMap {
     r0 = band * br;
     r1 = r0 + br < span ? r0 + br : span;
   }
+  // balanced: first row boundary (a multiple of align, < span) at or after unit position s
+  __device__ __forceinline__ void locate(long long s, int &col, int &row) const {
+    const int units = (span + align - 1) / align;
+    int c = (int)(s / units);
+    int u = (int)(s - (long long)c * units);
+    col = c;
+    row = u * align;
+  }
+  // run -> segments [(col, r0), (ce, re)): (col, r0 .. span), (col + 1, 0 .. span), ..., (ce, 0 .. re)
+  __device__ __forceinline__ void bounds(int run, int &col, int &r0, int &ce, int &re) const {
+    if (!bal) {
+      get(run, col, r0, re);
+      ce = col;
+      return;
+    }
+    const long long T = (long long)ncols * ((span + align - 1) / align);
+    locate(T * run / nparts, col, r0);
+    locate(T * (run + 1) / nparts, ce, re);
+  }
 
-  // host: split so that nruns() == resident when the columns allow it, bands >= min_rows
-  static RunMap make(long long ncols, int span, long long resident, int min_rows, int align) {
+  // host: banded split so that nruns() == resident when the columns allow it, bands >= min_rows;
+  // balanced: min(resident, ncols * span / min_rows) runs
+  static RunMap make(long long ncols, int span, long long resident, int min_rows, int align, bool balanced = false) {
     RunMap m;
     m.ncols = (int)ncols;
     m.span = span;
     m.align = align > 0 ? align : 1;
-    const int max_nb = span / (min_rows > 0 ? min_rows : 1) > 1 ? span / (min_rows > 0 ? min_rows : 1) : 1;
+    m.bal = 0;
+    m.nparts = 0;
+    const int mr = min_rows > 0 ? min_rows : 1;
+    const int max_nb = span / mr > 1 ? span / mr : 1;
     if (ncols >= resident) {
       m.nb_lo = 1;
       m.extra = 0;
@@ -226,9 +256,42 @@ struct RunMap {
       if (m.nb_lo >= max_nb) {
         m.nb_lo = max_nb;
         m.extra = 0;
+      } else if (balanced && m.extra != 0) {
+        // uneven bands: split evenly instead (whole columns when there are enough of them)
+        m.bal = 1;
+        long long units = ncols * ((span + m.align - 1) / m.align);
+        long long parts = resident;
+        const long long cap = ncols * span / mr;
+        if (parts > cap) parts = cap;
+        if (parts > units) parts = units;
+        m.nparts = (int)(parts < 1 ? 1 : parts);
       }
     }
     return m;
+  }
+  // mean rows per run (host: short-run decisions)
+  int mean_rows() const {
+    return bal ? (int)(((long long)ncols * span + nparts - 1) / nparts) : (span + nb_lo - 1) / nb_lo;
+  }
+};
+
+// The segments of this CTA's runs (runs blockIdx.x, blockIdx.x + gridDim.x, ...).
+struct RunIter {
+  const RunMap &m;
+  int run, col, r0, ce, re;
+  __device__ __forceinline__ explicit RunIter(const RunMap &map) : m(map), run((int)blockIdx.x), col(0), r0(0), ce(-1), re(0) {}
+  __device__ __forceinline__ bool next(int &c, int &a, int &b) {
+    while (!(col < ce || (col == ce && r0 < re))) {
+      if (run >= m.nruns()) return false;
+      m.bounds(run, col, r0, ce, re);
+      run += gridDim.x;
+    }
+    c = col;
+    a = r0;
+    b = col == ce ? re : m.span;
+    col++;
+    r0 = 0;
+    return true;
   }
 };
 

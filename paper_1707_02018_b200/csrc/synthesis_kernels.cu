@@ -140,10 +140,8 @@ __device__ __forceinline__ void syn_level_runs(const SynStreamParams<T, L> &p, u
   const bool act0 = tid < C::ITEMS0;
   const int m0c = tid % (C::TW / 2), grp0 = tid / (C::TW / 2);
 
-  const int nruns = p.runs.nruns();
-  for (int run = blockIdx.x; run < nruns; run += gridDim.x) {
-    int col, b0, b1;
-    p.runs.get(run, col, b0, b1);
+  int col, b0, b1;
+  for (RunIter itr(p.runs); itr.next(col, b0, b1);) {
     const int img = col / p.nstrips, strip = col - img * p.nstrips;
     if (b0 >= b1) continue;  // (uniform) empty trailing band
     const int tr0 = p.t00 + b0;  // even (bands are even)
@@ -453,8 +451,8 @@ cudaError_t make_syn_params(const SynthesisArgs &a, SynStreamParams<T, L> &p, bo
     e = kernel_resident(reinterpret_cast<const void *>(k_synth_stream<T, L, 0>), C::NT, C::smem_bytes(), &resident);
     if (e != cudaSuccess) return e;
     // one run per resident CTA when the columns allow it; even bands of >= 4 iterations
-    p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident, WL_SYN_MINROWS * C::G, 2);
-    const int band = (span0 + p.runs.nb_lo - 1) / p.runs.nb_lo;
+    p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident, WL_SYN_MINROWS * C::G, 2, balanced_runs());
+    const int band = p.runs.mean_rows();
     short_run = (band / 2 + C::H - 1) / C::G + 1 <= short_run_max(2);
   }
   if (short_run) {
@@ -464,7 +462,8 @@ cudaError_t make_syn_params(const SynthesisArgs &a, SynStreamParams<T, L> &p, bo
                           &resident4);
       if (e != cudaSuccess) return e;
     }
-    p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident4, WL_SYN_MINROWS * C4::G, 2);
+    p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident4, WL_SYN_MINROWS * C4::G, 2,
+                          balanced_runs());
     encode(C4::KCW, C4::G);
   } else {
     encode(C::KCW, C::G);

@@ -96,6 +96,14 @@ int match_tap_range(const double *lo, const double *hi, int L) {
   return 0;
 }
 
+bool balanced_runs() {
+  // measured on B200: balanced runs lose badly (cfg5 W* level 1 170 vs 108 us, grad 666 vs 561 us):
+  // strips that no longer stream the same rows at the same time break the DRAM page locality of
+  // their 0.5 KB box rows.  Banded unless WL_BALANCED is set (A/B).
+  static const bool v = getenv("WL_BALANCED") != nullptr;
+  return v;
+}
+
 bool multi_enabled() {
   // measured on B200 (graph replay): the cooperative multi-level tail lost to per-level PDL
   // launches (cfg4 W* 96 vs 80 us, cfg2 W* 26 vs 17 us): off unless WL_MULTI is set

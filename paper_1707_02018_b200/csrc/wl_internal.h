@@ -160,6 +160,9 @@ int match_tap_range(const double *lo, const double *hi, int L);
 bool zero_taps_enabled();
 // multi-level persistent launches for the coarse tails only when WL_MULTI is set (A-B switch)
 bool multi_enabled();
+// balanced (equal-row, column-spanning) runs for the analysis / synthesis level kernels (A/B: WL_BALANCED=1;
+// measured slower, see RunMap)
+bool balanced_runs();
 
 // PDL per launch site: kind 'A' / 'a' (analysis, long / short runs), 'S' / 's' (synthesis), 'b'
 // (blur).  WL_NO_PDL lists the kinds launched without it (an A/B switch; "AasSb" = none).
