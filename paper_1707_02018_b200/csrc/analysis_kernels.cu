@@ -136,22 +136,6 @@ struct ACfg {
   }
 };
 
-// Structural zeros of the filter pair: the nonzero tap range [l0, l1) of the lowpass
-// and [h0, h1) of the highpass array of the L-tap frame.  ZV = 0: every tap; the CDF 9/7 frame
-// (reading R4: a_lo = [0, h9], d_lo = [0, 0, h7, 0], unified highpass rule) has zeros at both ends.
-template <int L, int ZV>
-struct TapRange {
-  static constexpr int l0 = 0, l1 = L, h0 = 0, h1 = L;
-};
-template <>
-struct TapRange<10, 1> {  // dual filters (d_lo, d_hi): W* and W
-  static constexpr int l0 = 2, l1 = 9, h0 = 0, h1 = 9;
-};
-template <>
-struct TapRange<10, 2> {  // analysis filters (a_lo, a_hi): W-dagger and (W-dagger)*
-  static constexpr int l0 = 1, l1 = 10, h0 = 1, h1 = 8;
-};
-
 template <typename T, int L>
 struct AnaStreamParams {
   using P = typename Pair<T>::t;
@@ -608,6 +592,10 @@ cudaError_t make_ana_params(const AnalysisArgs &a, AnaStreamParams<T, L> &p, boo
 
 template <typename T, int L, bool FU, int ZV = 0>
 cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
+  if (!FU && sizeof(T) == 4) {  // zero-extension levels: the register-ring kernel
+    cudaError_t e = cudaSuccess;
+    if (launch_analysis_ring(WL_F32, a, s, &e)) return e;
+  }
   using C = ACfg<T, L, 0, FU>;
   using C4 = ACfg<T, L, 4, FU>;
   AnaStreamParams<T, L> p;

@@ -121,6 +121,26 @@ __device__ __forceinline__ P splat2(T v) {
 
 }  // namespace wl
 
+namespace wl {
+
+// Structural zeros of the filter pair: the nonzero tap range [l0, l1) of the lowpass
+// and [h0, h1) of the highpass array of the L-tap frame.  ZV = 0: every tap; the CDF 9/7 frame
+// (reading R4: a_lo = [0, h9], d_lo = [0, 0, h7, 0], unified highpass rule) has zeros at both ends.
+template <int L, int ZV>
+struct TapRange {
+  static constexpr int l0 = 0, l1 = L, h0 = 0, h1 = L;
+};
+template <>
+struct TapRange<10, 1> {  // dual filters (d_lo, d_hi): W* and W
+  static constexpr int l0 = 2, l1 = 9, h0 = 0, h1 = 9;
+};
+template <>
+struct TapRange<10, 2> {  // analysis filters (a_lo, a_hi): W-dagger and (W-dagger)*
+  static constexpr int l0 = 1, l1 = 10, h0 = 1, h1 = 8;
+};
+
+}  // namespace wl
+
 // ---------------------------------------------------------------- mbarrier + TMA (sm_90+)
 namespace wl {
 

@@ -94,6 +94,10 @@ cudaError_t launch_blur_residual(int dtype, const BlurArgs &a, cudaStream_t s);
 // aligned buffers.  Returns false (nothing launched) when the arguments are outside that domain;
 // otherwise launches and stores the launch status in *err.
 bool launch_blur_ring(int dtype, const BlurArgs &a, bool residual, cudaStream_t s, cudaError_t *err);
+// Register-ring analysis level (analysis_ring_kernels.cu): fp32, zero extension (W* under zero /
+// symmetric BC, W-dagger under zero BC), no FISTA epilogue.  Returns false (nothing launched)
+// outside that domain; otherwise launches and stores the launch status in *err.
+bool launch_analysis_ring(int dtype, const AnalysisArgs &a, cudaStream_t s, cudaError_t *err);
 cudaError_t launch_zero(void *ptr, size_t bytes, cudaStream_t s);
 // FISTA pieces (fista_kernels.cu); n = elements per call (batch * p_alloc for the update)
 // Example 2: batched valid cross-correlation out_b[i] = sum_{j<ta} a_b[j] b_b[i+j]
