@@ -260,6 +260,27 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
         }
         return true;
       }
+      // symmetric extensions, blocks reaching past the top / bottom or into the weighted rows: one
+      // bulk copy per row from its reflected source row (P:82 applied to rows), columns clipped to
+      // the image (a row end that is not 16-byte aligned copied by the lane); the outside columns
+      // are mirrored and the (E_sym^dagger)* column weights applied in shared memory after it
+      // lands, the row weights to the B-stage output.  (TMA row boxes would need 128-byte aligned
+      // shared rows.)
+      if (p.tma && (p.ext == EXT_SYM || p.ext == EXT_SYM_PADJ) && (cols_in || sym_fix)) {
+        if (tid < 32) {  // warp 0: lane r copies rows r, r + 32, ...
+          const int a0 = max(cbox, 0), e = min(cbox + C::UW, p.n1), e4 = max(a0, e / VEC * VEC);
+          if (tid == 0) mbar_arrive_expect_tx(bar + sl, (unsigned)(GI * (e4 - a0) * sizeof(T)));
+          __syncwarp();
+          fence_proxy_async();
+          for (int r = tid; r < GI; r += 32) {
+            const T *srow = in + (long long)refl_inf(r_in + r, p.n0) * p.in_pitch;
+            T *drow = dst0 + r * C::UP - cbox;
+            if (e4 > a0) bulk_load(drow + a0, srow + a0, (unsigned)((e4 - a0) * sizeof(T)), bar + sl);
+            for (int c = e4; c < e; c++) drow[c] = srow[c];  // a row end that is not 16-byte aligned
+          }
+        }
+        return true;
+      }
       for (int idx = tid; idx < GI * C::NV; idx += C::NT) {
         const int r = idx / C::NV, v = idx - r * C::NV;
         T wr;
@@ -304,42 +325,48 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
     for (int it = -1; it < nblk; it++) {
       const int slot = (it + 1) % C::NS;
       cp_async_wait_group<C::NS - 2>();  // this thread's gathers of block it are done
-      if ((armed >> slot) & 1) {
+      const bool async_blk = (armed >> slot) & 1;  // block it came by TMA / bulk copies
+      if (async_blk) {
         mbar_wait(bar + slot, (phase >> slot) & 1);
         phase ^= 1u << slot;
       }
       __syncthreads();  // (1) block it landed; the history move of it-1 is done
-      if (sym_fix && p.tma) {
-        const int r_it = 2 * (kr0 + it * G);
+      bool padj_rows = false;  // async (E_sym^dagger)* block with weighted rows
+      const int r_blk = 2 * (kr0 + it * G);
+      if (async_blk && (p.ext == EXT_SYM || p.ext == EXT_SYM_PADJ)) {
         const int wpad = p.ext == EXT_SYM_PADJ ? L - 1 : 0;
-        if (r_it >= wpad && r_it + GI <= p.n0 - wpad) {  // block it came by TMA: mirror its outside columns
-          T *ub = ubuf + slot * GI * C::UP;
-          const int per = fix_nl + fix_nr;
-          for (int idx = tid; idx < GI * per; idx += C::NT) {
-            const int r = idx / per, k = idx - r * per;
-            const int g = k < fix_nl ? cbox + k : fix_r0 + (k - fix_nl);
-            const int src = g < 0 ? -1 - g : 2 * p.n1 - 1 - g;
-            ub[r * C::UP + (g - cbox)] = ub[r * C::UP + (src - cbox)];
+        const bool blk_rows_in = r_blk >= wpad && r_blk + GI <= p.n0 - wpad;
+        T *ub = ubuf + slot * GI * C::UP;
+        if (sym_fix) {
+          // one pass: thread -> one source column s near an edge (every rstep-th row); it writes its
+          // mirror images [cbox, 0) / [n1, fix_lim) (half-point reflection) and, for
+          // (E_sym^dagger)* = E_sym diag(1/c), scales s and its images by 1/c_s
+          // (c = 1 + [s < L-1] + [s >= n-L+1]).  Reading each source once keeps it race-free.
+          const int Lw = p.ext == EXT_SYM_PADJ ? L - 1 : 0;
+          const int a = min(max(Lw, fix_nl), p.n1);              // left sources [0, a)
+          const int b0 = max(a, p.n1 - max(Lw, fix_nr));          // right sources [b0, n1)
+          const int la0 = max(0, cbox), la1 = min(a, cbox + C::UW);
+          const int ra0 = max(b0, cbox), ra1 = min(p.n1, cbox + C::UW);
+          const int nl = max(0, la1 - la0), nr = max(0, ra1 - ra0), per = nl + nr;
+          if (per > 0) {
+            const int rstep = C::NT / per > 0 ? C::NT / per : 1, k = tid % per;
+            const int sc = k < nl ? la0 + k : ra0 + (k - nl);
+            const int gl = -1 - sc, gr = 2 * p.n1 - 1 - sc;
+            const bool wl = gl >= cbox, wr = gr < fix_lim && gr < cbox + C::UW;
+            const int c = Lw ? 1 + (sc < Lw ? 1 : 0) + (sc >= p.n1 - Lw ? 1 : 0) : 1;
+            const T wgt = T(1) / T(c);
+            for (int r = tid / per; r < GI && tid < rstep * per; r += rstep) {
+              T *row = ub + r * C::UP - cbox;
+              const T v = row[sc] * wgt;
+              if (c > 1) row[sc] = v;
+              if (wl) row[gl] = v;
+              if (wr) row[gr] = v;
+            }
           }
           __syncthreads();
-          if (p.ext == EXT_SYM_PADJ) {
-            // (E_sym^dagger)* = E_sym diag(1/c): every column within L-1 of an edge, inside or
-            // mirrored, times 1/c of its source (c = 1 + [s < L-1] + [s >= n-L+1]); rows are all
-            // weight 1 here
-            const int Lp = L - 1;
-            const int la = cbox, lb = min(Lp, cbox + C::UW);               // left set [la, lb)
-            const int ra = max(cbox, p.n1 - Lp), rb = fix_lim;             // right set [ra, rb)
-            const int nl = max(0, lb - la), nr = max(0, rb - ra), per2 = nl + nr;
-            for (int idx = tid; idx < GI * per2; idx += C::NT) {
-              const int r = idx / per2, k = idx - r * per2;
-              const int g = k < nl ? la + k : ra + (k - nl);
-              const int src = g < 0 ? -1 - g : (g >= p.n1 ? 2 * p.n1 - 1 - g : g);
-              const int c = 1 + (src < Lp ? 1 : 0) + (src >= p.n1 - Lp ? 1 : 0);
-              if (c > 1) ub[r * C::UP + (g - cbox)] *= T(1) / T(c);
-            }
-            __syncthreads();
-          }
         }
+        // rows of (E_sym^dagger)*: applied to the B-stage output of the row (row_w below)
+        padj_rows = p.ext == EXT_SYM_PADJ && !blk_rows_in;
       }
       {
         const int nb = it + C::NS - 1;  // its slot held block it-1, consumed before (1)
@@ -363,6 +390,15 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
           const P f = p.fb[j];
 #pragma unroll
           for (int k = 0; k < V; k++) acc[k] = fma2(f, splat2<P>(win[C::SHIFT + 2 * k + L - 1 - j]), acc[k]);
+        }
+        if (padj_rows) {  // (E_sym^dagger)* row weight 1/c of the row's source (linear: scale the output)
+          const int sr = refl_inf(r_blk + rowB, p.n0), Lp = L - 1;
+          const int c = 1 + (sr < Lp ? 1 : 0) + (sr >= p.n0 - Lp ? 1 : 0);
+          if (c > 1) {
+            const P wv = splat2<P>(T(1) / T(c));
+#pragma unroll
+            for (int k = 0; k < V; k++) acc[k] = mul2(acc[k], wv);
+          }
         }
         T lo[V], hi[V];
 #pragma unroll
