@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -231,6 +232,11 @@ wl_status run_analysis(const wl_plan *p, int64_t batch, const void *img, void *x
   return WL_OK;
 }
 
+bool full_fold() {
+  static const bool v = getenv("WL_FULL_FOLD") != nullptr;  // A/B: synthesize the whole frame, fold it all
+  return v;
+}
+
 // synthesis chain (W) ------------------------------------------------------------
 // Multi-level upsample-convolve chain, coarse -> fine.  transpose_of_analysis = false: W
 // (dual filters; crop / periodic / weighted EDAG fold); true: (W-dagger)* (analysis filters;
@@ -269,9 +275,11 @@ wl_status run_synthesis(const wl_plan *p, int64_t batch, const void *x, void *im
     }
     if (sym) {
       // synthesize onto [-L', n+L') per axis, then fold: E_sym^dagger (W of EDAG) or
-      // E_sym^T ((W-dagger)* under symmetric BC)
-      // U columns start one position earlier, at t = -L (even): output column pairs then sit at
-      // even U indices and the synthesis stores them as aligned pairs (the extra column is 0)
+      // E_sym^T ((W-dagger)* under symmetric BC).  U columns start one position earlier, at t = -L
+      // (even): output column pairs then sit at even U indices and stay aligned pairs.  Split
+      // output: the in-image positions go straight to the level's output, U keeps only the frame
+      // outside it, and the fold touches the L'-wide border only (WL_FULL_FOLD: the whole frame
+      // in U and a full-image fold pass, A/B).
       int64_t ep = round_up(n1 + 2 * Lp + 1, 16 / p->es);
       a.out = ws + L.e;
       a.out_pitch = ep;
@@ -280,6 +288,14 @@ wl_status run_synthesis(const wl_plan *p, int64_t batch, const void *x, void *im
       a.N1 = (int)(n1 + 2 * Lp + 1);
       a.o0 = -Lp;
       a.o1 = -Lp - 1;
+      const bool split = !full_fold();
+      if (split) {
+        a.y = out.ptr;
+        a.y_pitch = out.pitch;
+        a.y_bstride = out.bstride;
+        a.yn0 = (int)n0;
+        a.yn1 = (int)n1;
+      }
       cudaError_t e = launch_synthesis(p->dtype, a, s);
       if (e != cudaSuccess) return cuda_fail(e, "synthesis level launch");
       FoldArgs f;
@@ -295,6 +311,7 @@ wl_status run_synthesis(const wl_plan *p, int64_t batch, const void *x, void *im
       f.weighted = transpose_of_analysis ? 0 : 1;
       f.batch = (int)batch;
       f.col_off = 1;
+      f.border_only = split ? 1 : 0;
       e = launch_fold(p->dtype, f, s);
       if (e != cudaSuccess) return cuda_fail(e, "fold launch");
     } else {

@@ -113,6 +113,9 @@ struct SynStreamParams {
   int nstrips;
   RunMap runs;               // (image, strip) columns x bands of extended output rows
   int tma, vec_store;
+  T *y;                      // split output (symmetric folds): in-image positions go to y
+  long long y_pitch, y_bstride;
+  int split, yn0, yn1, y_vec;
   P g1lo[H_MAX], g1hi[H_MAX];  // S1 tap pairs (g[2q+1], g[2q])
   P e_lo[H_MAX], o_lo[H_MAX];  // S0 broadcast taps (g[2q+1], g[2q+1]) and (g[2q], g[2q])
   P e_hi[H_MAX], o_hi[H_MAX];
@@ -120,7 +123,7 @@ struct SynStreamParams {
 
 // One level's runs (the body of k_synth_stream; k_synth_multi calls it once per level of the
 // coarse head of a W chain).  `phase` carries the stage barriers' parities across calls.
-template <typename T, int L, int NS, int ZV = 0>
+template <typename T, int L, int NS, int ZV = 0, bool SPLIT = false>
 __device__ __forceinline__ void syn_level_runs(const SynStreamParams<T, L> &p, unsigned char *smem_raw,
                                                unsigned &phase) {
   using C = SCfg<T, L, NS>;
@@ -303,13 +306,51 @@ __device__ __forceinline__ void syn_level_runs(const SynStreamParams<T, L> &p, u
         }
         // fast path: every output row of the item lies in the run and the image, pair stores
         const int t_lo = 2 * sb, t_hi = 2 * (sb + VC);  // [t_lo, t_hi)
-        if (vec_ok && sb >= s_first && sb + VC - 1 <= s_last && t_lo >= tr0 && t_hi <= tr1 && t_lo - p.o0 >= 0 &&
-            t_hi - p.o0 <= p.N0) {
+        const bool run_in = sb >= s_first && sb + VC - 1 <= s_last && t_lo >= tr0 && t_hi <= tr1;
+        // split output: pairs inside the image go to y, the rest to out (U's border frame)
+        const int t1 = oc + p.o1;  // extended column of the pair (even)
+        const bool pair_y = SPLIT && t1 >= 0 && t1 + 1 < p.yn1;
+        const bool pair_u = !SPLIT || t1 + 1 < 0 || t1 >= p.yn1;
+        if (SPLIT && pair_y && p.y_vec && run_in && t_lo >= 0 && t_hi <= p.yn0) {
+          T *op = p.y + (long long)img * p.y_bstride + (long long)t_lo * p.y_pitch + t1;
+#pragma unroll
+          for (int v = 0; v < VC; v++) {
+            *reinterpret_cast<P *>(op + (2 * v) * p.y_pitch) = e[v];
+            *reinterpret_cast<P *>(op + (2 * v + 1) * p.y_pitch) = o[v];
+          }
+        } else if ((pair_u || t_hi <= 0 || t_lo >= p.yn0) && vec_ok && run_in && t_lo - p.o0 >= 0 &&
+                   t_hi - p.o0 <= p.N0) {
           T *op = out + (long long)(t_lo - p.o0) * p.out_pitch + oc;
 #pragma unroll
           for (int v = 0; v < VC; v++) {
             *reinterpret_cast<P *>(op + (2 * v) * p.out_pitch) = e[v];
             *reinterpret_cast<P *>(op + (2 * v + 1) * p.out_pitch) = o[v];
+          }
+        } else if (SPLIT) {  // split output, item at a band end or the image border: route per row
+#pragma unroll
+          for (int v = 0; v < VC; v++) {
+            const int s = sb + v;
+            if (s < s_first || s > s_last) continue;
+#pragma unroll
+            for (int par = 0; par < 2; par++) {
+              const int t = 2 * s + par;
+              const int orow = t - p.o0;
+              if (t < tr0 || t >= tr1 || orow < 0 || orow >= p.N0) continue;
+              const P val = par ? o[v] : e[v];
+              const bool row_y = t >= 0 && t < p.yn0;
+              T *yp = p.y + (long long)img * p.y_bstride + (long long)t * p.y_pitch + t1;
+              T *op = out + (long long)orow * p.out_pitch + oc;
+              if (row_y && pair_y && p.y_vec) {
+                *reinterpret_cast<P *>(yp) = val;
+              } else if ((!row_y || pair_u) && vec_ok) {
+                *reinterpret_cast<P *>(op) = val;
+              } else {  // a pair straddling the image's right edge (odd n1)
+                if (row_y && t1 >= 0 && t1 < p.yn1) yp[0] = val.x;
+                else if (oc >= 0 && oc < p.N1) op[0] = val.x;
+                if (row_y && t1 + 1 >= 0 && t1 + 1 < p.yn1) yp[1] = val.y;
+                else if (oc + 1 >= 0 && oc + 1 < p.N1) op[1] = val.y;
+              }
+            }
           }
         } else {
 #pragma unroll
@@ -348,8 +389,9 @@ __device__ __forceinline__ void syn_level_runs(const SynStreamParams<T, L> &p, u
   }
 }
 
-template <typename T, int L, int NS, int ZV = 0>
-__global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 768 / SCfg<T, L>::NT : 1)
+// (the split variant is capped at the plain kernel's register count so it keeps its CTAs per SM)
+template <typename T, int L, int NS, int ZV = 0, bool SPLIT = false>
+__global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? (SPLIT ? 1024 : 768) / SCfg<T, L>::NT : 1)
     k_synth_stream(const __grid_constant__ SynStreamParams<T, L> p) {
   using C = SCfg<T, L, NS>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -361,7 +403,7 @@ __global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? 768 / SCfg<T,
   pdl_launch_dependents();
   pdl_wait();  // the previous kernel of the stream wrote our inputs
   unsigned phase = 0;
-  syn_level_runs<T, L, NS, ZV>(p, smem_raw, phase);
+  syn_level_runs<T, L, NS, ZV, SPLIT>(p, smem_raw, phase);
 }
 
 // The coarse head of a W chain (levels J .. j0, coarse -> fine) in one persistent cooperative
@@ -433,6 +475,15 @@ cudaError_t make_syn_params(const SynthesisArgs &a, SynStreamParams<T, L> &p, bo
   p.t01 = 2 * C::VEC * (int)std::floor((double)a.o1 / (2.0 * C::VEC));
   p.vec_store = (a.o1 % 2 == 0) && (a.out_pitch % 2 == 0) && (a.out_bstride % 2 == 0) &&
                 (reinterpret_cast<uintptr_t>(a.out) % (2 * sizeof(T)) == 0);
+  p.y = static_cast<T *>(a.y);
+  p.split = a.y != nullptr;
+  p.y_pitch = a.y_pitch;
+  p.y_bstride = a.y_bstride;
+  p.yn0 = a.yn0;
+  p.yn1 = a.yn1;
+  // pairs start at even extended columns t1: 8-byte aligned in y when its pitch is even
+  p.y_vec = p.split && (a.y_pitch % 2 == 0) && (a.y_bstride % 2 == 0) &&
+            (reinterpret_cast<uintptr_t>(a.y) % (2 * sizeof(T)) == 0);
   for (int q = 0; q < C::H; q++) {
     p.g1lo[q].x = T(a.lo[2 * q + 1]); p.g1lo[q].y = T(a.lo[2 * q]);
     p.g1hi[q].x = T(a.hi[2 * q + 1]); p.g1hi[q].y = T(a.hi[2 * q]);
@@ -480,18 +531,19 @@ cudaError_t launch_synth_stream_t(const SynthesisArgs &a, cudaStream_t s) {
   cudaError_t e = make_syn_params<T, L>(a, p, short_run, false);
   if (e != cudaSuccess) return e;
   long long resident = 0;
+  // split outputs (symmetric folds) take their own instantiation: the routing costs registers
+  auto kshort = p.split ? k_synth_stream<T, L, 4, ZV, true> : k_synth_stream<T, L, 4, ZV, false>;
+  auto klong = p.split ? k_synth_stream<T, L, 0, ZV, true> : k_synth_stream<T, L, 0, ZV, false>;
   if (short_run) {
-    e = kernel_resident(reinterpret_cast<const void *>(k_synth_stream<T, L, 4, ZV>), C4::NT, C4::smem_bytes(),
-                        &resident);
+    e = kernel_resident(reinterpret_cast<const void *>(kshort), C4::NT, C4::smem_bytes(), &resident);
     if (e != cudaSuccess) return e;
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
-    e = launch_pdl(k_synth_stream<T, L, 4, ZV>, grid, C4::NT, C4::smem_bytes(), s, p, 's');
+    e = launch_pdl(kshort, grid, C4::NT, C4::smem_bytes(), s, p, 's');
   } else {
-    e = kernel_resident(reinterpret_cast<const void *>(k_synth_stream<T, L, 0, ZV>), C::NT, C::smem_bytes(),
-                        &resident);
+    e = kernel_resident(reinterpret_cast<const void *>(klong), C::NT, C::smem_bytes(), &resident);
     if (e != cudaSuccess) return e;
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
-    e = launch_pdl(k_synth_stream<T, L, 0, ZV>, grid, C::NT, C::smem_bytes(), s, p, 'S');
+    e = launch_pdl(klong, grid, C::NT, C::smem_bytes(), s, p, 'S');
   }
   g_launches++;
   if (e != cudaSuccess) return e;

@@ -55,6 +55,11 @@ struct SynthesisArgs {
   const double *lo, *hi;
   int L;
   int batch;
+  // split output (symmetric folds): extended positions inside the image, t in [0, yn0) x [0, yn1),
+  // go to y (the fold's output, written in place of its interior) and only the rest to out
+  void *y = nullptr;
+  int64_t y_pitch = 0, y_bstride = 0;
+  int yn0 = 0, yn1 = 0;
 };
 
 struct FoldArgs {  // y = diag(1/c) E_sym^T U per axis (weighted: W of SYMMETRIC_EDAG) or E_sym^T U
@@ -66,7 +71,11 @@ struct FoldArgs {  // y = diag(1/c) E_sym^T U per axis (weighted: W of SYMMETRIC
   int weighted;                  // 1: E_sym^dagger = diag(1/c) E_sym^T; 0: E_sym^T ((W-dagger)*)
   int batch;
   int col_off = 0;               // U column of extended position t is t + Lp + col_off
+  int border_only = 0;           // 1: y already holds U's in-image part (split synthesis); fold the
+                                 //    L'-wide border only, reading the outside positions from U
 };
+
+
 
 struct BlurArgs {
   const void *in;
