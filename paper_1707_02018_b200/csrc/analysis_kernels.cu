@@ -281,6 +281,33 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
         }
         return true;
       }
+      // periodic extension, blocks that wrap (edge strips, top / bottom): per row one bulk copy of the
+      // in-image columns (warp 0's lanes) and cp.async of the wrapped 16-byte chunks at either end (all
+      // threads), from the wrapped source row (reading R2: indices mod n) -- every box column
+      // filled, no shared-memory fix
+      if (p.tma && p.ext == EXT_PER && p.n1 % VEC == 0 && -cbox <= p.n1 && cbox + C::UW - p.n1 <= p.n1) {
+        const int a0 = max(cbox, 0), e = min(cbox + C::UW, p.n1);
+        const int nl = max(0, -cbox) / VEC, nr = max(0, cbox + C::UW - p.n1) / VEC;  // wrapped chunks
+        auto row_of = [&](int r) {
+          int sr = (r_in + r) % p.n0;
+          if (sr < 0) sr += p.n0;
+          return in + (long long)sr * p.in_pitch;
+        };
+        if (tid < 32) {
+          if (tid == 0) mbar_arrive_expect_tx(bar + sl, (unsigned)(GI * (e - a0) * sizeof(T)));
+          __syncwarp();
+          fence_proxy_async();
+          for (int r = tid; r < GI; r += 32)
+            bulk_load(dst0 + r * C::UP + (a0 - cbox), row_of(r) + a0, (unsigned)((e - a0) * sizeof(T)), bar + sl);
+        }
+        for (int idx = tid; idx < GI * (nl + nr); idx += C::NT) {
+          const int r = idx / (nl + nr), c = idx - r * (nl + nr);
+          const int col = c < nl ? cbox + VEC * c : p.n1 + VEC * (c - nl);  // box column of the chunk
+          const int srcc = c < nl ? col + p.n1 : col - p.n1;
+          cp_async16(dst0 + r * C::UP + (col - cbox), row_of(r) + srcc);
+        }
+        return true;
+      }
       for (int idx = tid; idx < GI * C::NV; idx += C::NT) {
         const int r = idx / C::NV, v = idx - r * C::NV;
         T wr;
