@@ -56,7 +56,13 @@ __device__ __forceinline__ unsigned smid() {
 template <int HW, bool RESID>
 struct RingCfg {
   static_assert(2 * HW + 1 <= kRing, "ring too short for this PSF");
-  static constexpr int NP = 128;          // column pairs per strip
+#ifndef WL_RING_NB
+#define WL_RING_NB 2
+#endif
+  // TMA boxes per operand, 64 column pairs (2 warps) each.  A/B on B200 (cfg5 residual): 2 boxes
+  // (128 threads, 4 CTAs per SM) 251 us; 4 boxes (256 threads, 2 CTAs, half the strip halo) 258 us
+  static constexpr int NB = WL_RING_NB;
+  static constexpr int NP = 64 * NB;      // column pairs per strip
   static constexpr int NT = NP;           // one thread per pair; it runs both stages
   static constexpr int G = 5;             // rows per group (divides kRing)
 #ifndef WL_RING_S
@@ -71,18 +77,18 @@ struct RingCfg {
   // the first output to window position 1
   static constexpr int S0 = RESID ? 0 : (HW & 1);
   static constexpr int NWIN = 2 * HW + 2 + 2 * S0;
-  static constexpr int UBOX = round_up_c(130 + NWIN, 4);  // box 0: [0, UBOX), box 1: [128, 128 + UBOX)
+  static constexpr int UBOX = round_up_c(130 + NWIN, 4);  // box b: [128 b, 128 b + UBOX)
   static constexpr int BBOX = 132;
   // one (stage, box) region holds G dense rows (a G-row TMA box), 128-byte aligned
   static constexpr int UREG = round_up_c(G * UBOX * 4, 128) / 4;
   static constexpr int BREG = round_up_c(G * BBOX * 4, 128) / 4;
-  static constexpr size_t OFF_U = 0;  // [S][2 boxes][UREG]
-  static constexpr size_t OFF_B = OFF_U + (size_t)S * 2 * UREG * 4;  // [S][2][BREG]
+  static constexpr size_t OFF_U = 0;  // [S][NB boxes][UREG]
+  static constexpr size_t OFF_B = OFF_U + (size_t)S * NB * UREG * 4;  // [S][NB][BREG]
   static constexpr int NR = 2;            // r row blocks (double buffer: one barrier per group)
-  static constexpr size_t OFF_R = OFF_B + (RESID ? (size_t)S * 2 * BREG * 4 : 0);  // [NR][G][NC]
+  static constexpr size_t OFF_R = OFF_B + (RESID ? (size_t)S * NB * BREG * 4 : 0);  // [NR][G][NC]
   static constexpr size_t OFF_BAR = OFF_R + (RESID ? (size_t)NR * G * NC * 4 : 0);
   static constexpr size_t SMEM = OFF_BAR + S * sizeof(uint64_t);  // mbarriers full[S] (TMA landed)
-  static constexpr unsigned TX = 2u * G * (UBOX + (RESID ? BBOX : 0)) * 4u;  // bytes per group
+  static constexpr unsigned TX = (unsigned)NB * G * (UBOX + (RESID ? BBOX : 0)) * 4u;  // bytes per group
 };
 
 template <int HW>
@@ -164,10 +170,10 @@ __device__ __forceinline__ float2 vring(const float2 (&ring)[kRing], int nw, con
 }
 
 #ifndef WL_RING_MINB
-#define WL_RING_MINB 4
+#define WL_RING_MINB (8 / WL_RING_NB)
 #endif
 template <int HW, bool RESID>
-__global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_constant__ RingParams<HW> p) {
+__global__ void __launch_bounds__(64 * WL_RING_NB, WL_RING_MINB) k_blur_ring(const __grid_constant__ RingParams<HW> p) {
   using C = RingCfg<HW, RESID>;
   constexpr int G = C::G, S = C::S, NWIN = C::NWIN, S0 = C::S0;
   extern __shared__ __align__(128) unsigned char sm[];
@@ -176,7 +182,7 @@ __global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_co
   float *rbuf = reinterpret_cast<float *>(sm + C::OFF_R);  // [2][G][NC]   r rows (residual)
   uint64_t *full = reinterpret_cast<uint64_t *>(sm + C::OFF_BAR);
   const int tid = threadIdx.x;
-  const int box = tid >> 6;  // warps 0-1 read box 0, warps 2-3 box 1
+  const int box = tid >> 6;  // warps 2b, 2b+1 read box b
   // stage regions start finite: edge-group copies leave the out-of-image columns untouched
   for (int i = tid; i < (int)(C::OFF_BAR / 16); i += C::NT)
     reinterpret_cast<float4 *>(sm)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -241,7 +247,8 @@ __global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_co
       if (x >= ulo && x < ulo + 62 + NWIN && x >= box * 128 && x < box * 128 + C::UBOX) {
         const int sx = refl_inf(c, w) - ustart;
         ufix_t = box * C::UREG + x - box * 128;
-        ufix_s = sx < C::UBOX ? sx : C::UREG + sx - 128;
+        const int sbx = min(C::NB - 1, sx / 128);  // a box holding the source column
+        ufix_s = sbx * C::UREG + sx - sbx * 128;
       }
       const int xr = c - col1;                               // its r index over [0, NC)
       if (RESID && xr >= wq && xr < wq + 62 + NWIN && xr < C::NC) {
@@ -264,23 +271,25 @@ __global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_co
     double fsum = 0.0;
 
     __syncthreads();  // the previous run's readers of every buffer are done
-    // group kk -> stage (gbase + kk) % S: lane 0 of warp `part` loads operand box `part` (u box 0,
-    // u box 1, b box 0, b box 1); groups inside the image take one G-row TMA box, edge groups
+    // group kk -> stage (gbase + kk) % S: lane 0 of warp `part` loads operand box `part` (u boxes 0 .. NB-1,
+    // then b boxes 0 .. NB-1); groups inside the image take one G-row TMA box, edge groups
     // row-wise bulk copies; part 0 also arms the stage's barrier with the group's bytes
     auto issue_part = [&](int kk, int part) {
       const int st = (gbase + kk) % S;
       const int yu = urow0 + kk * G, yb = brow0 + kk * G;
       const bool tu = yu >= 0 && yu + G <= h, tb = yb >= 0 && yb + G <= h;
       if (part == 0) {
-        unsigned bytes = ring_box_bytes(tu, G, ustart, C::UBOX, w) + ring_box_bytes(tu, G, ustart + 128, C::UBOX, w);
-        if (RESID)
-          bytes += ring_box_bytes(tb, G, bstart, C::BBOX, w) + ring_box_bytes(tb, G, bstart + 128, C::BBOX, w);
+        unsigned bytes = 0;
+        for (int bx = 0; bx < C::NB; bx++) {
+          bytes += ring_box_bytes(tu, G, ustart + 128 * bx, C::UBOX, w);
+          if (RESID) bytes += ring_box_bytes(tb, G, bstart + 128 * bx, C::BBOX, w);
+        }
         mbar_arrive_expect_tx(full + st, bytes);
       }
-      if (part >= 2 && !RESID) return;
-      const bool isu = part < 2, inside = isu ? tu : tb;
-      const int bx = part & 1;
-      float *dst = isu ? ubase + (st * 2 + bx) * C::UREG : bbase + (st * 2 + bx) * C::BREG;
+      if (part >= C::NB && !RESID) return;
+      const bool isu = part < C::NB, inside = isu ? tu : tb;
+      const int bx = isu ? part : part - C::NB;
+      float *dst = isu ? ubase + (st * C::NB + bx) * C::UREG : bbase + (st * C::NB + bx) * C::BREG;
       const int cs = (isu ? ustart : bstart) + 128 * bx;
       fence_proxy_async();
       if (inside)
@@ -300,7 +309,7 @@ __global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_co
         const unsigned g = gbase + k;
         const int st = g % S;
         mbar_wait(full + st, (g / S) & 1);
-        float *ust = ubase + st * 2 * C::UREG;
+        float *ust = ubase + st * C::NB * C::UREG;
         if (uedge) {
           if (ufix_t >= 0) {  // all G loads first, then the stores: one shared-memory latency
             float v[G];
@@ -312,7 +321,7 @@ __global__ void __launch_bounds__(128, WL_RING_MINB) k_blur_ring(const __grid_co
           __syncwarp();
         }
         const float *ub = ust + widx;
-        const float *bb = bbase + st * 2 * C::BREG + bidx;
+        const float *bb = bbase + st * C::NB * C::BREG + bidx;
         float *rw = rbuf + (k & 1) * G * C::NC;
         float2 fa = make_float2(0.f, 0.f);
         // output row of step 0 of this group (stage 1 for R, stage 2 for the residual)
