@@ -689,6 +689,17 @@ cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
 template <typename T, int L, int ZV = 0>
 cudaError_t launch_ana_chain_t(const AnalysisArgs *a, int n, cudaStream_t s) {
   using C4 = ACfg<T, L, 4, false>;
+  {  // the coarse levels that fit in one CTA's shared memory: one launch, one CTA per image
+    const int dtype = sizeof(T) == 8 ? WL_F64 : WL_F32;
+    const int i0 = small_analysis_start(dtype, a, n);
+    if (i0 < n) {
+      for (int i = 0; i < i0; i++) {
+        cudaError_t e = launch_ana_stream_t<T, L, false, ZV>(a[i], s);
+        if (e != cudaSuccess) return e;
+      }
+      return launch_analysis_small(dtype, a + i0, n - i0, s);
+    }
+  }
   int first_short = n;
   for (int i = 0; i < n && first_short == n; i++) {
     AnaStreamParams<T, L> p;

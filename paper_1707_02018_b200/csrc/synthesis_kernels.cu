@@ -555,6 +555,19 @@ cudaError_t launch_synth_stream_t(const SynthesisArgs &a, cudaStream_t s) {
 template <typename T, int L, int ZV = 0>
 cudaError_t launch_syn_chain_t(const SynthesisArgs *a, int n, cudaStream_t s) {
   using C4 = SCfg<T, L, 4>;
+  {  // the coarse levels that fit in one CTA's shared memory: one launch, one CTA per image
+    const int dtype = sizeof(T) == 8 ? WL_F64 : WL_F32;
+    const int i1 = small_synthesis_end(dtype, a, n);
+    if (i1 > 0) {
+      cudaError_t e = launch_synthesis_small(dtype, a, i1, s);
+      if (e != cudaSuccess) return e;
+      for (int i = i1; i < n; i++) {
+        e = launch_synth_stream_t<T, L, ZV>(a[i], s);
+        if (e != cudaSuccess) return e;
+      }
+      return cudaSuccess;
+    }
+  }
   int nshort = 0;  // coarse levels are short first: count the leading short ones
   for (int i = 0; i < n; i++) {
     SynStreamParams<T, L> p;

@@ -107,6 +107,14 @@ bool launch_blur_ring(int dtype, const BlurArgs &a, bool residual, cudaStream_t 
 // symmetric BC, W-dagger under zero BC), no FISTA epilogue.  Returns false (nothing launched)
 // outside that domain; otherwise launches and stores the launch status in *err.
 bool launch_analysis_ring(int dtype, const AnalysisArgs &a, cudaStream_t s, cudaError_t *err);
+// Small-level kernels (small_kernels.cu): the coarse levels whose input fits in one CTA's shared
+// memory run as one launch with one CTA per image.  small_analysis_start returns the first index
+// of a (fine -> coarse) chain that the small kernel takes (n: none); small_synthesis_end the end of
+// the (coarse -> fine) prefix it takes (0: none).  WL_NO_SMALL disables both (A/B).
+int small_analysis_start(int dtype, const AnalysisArgs *a, int n);
+cudaError_t launch_analysis_small(int dtype, const AnalysisArgs *a, int n, cudaStream_t s);
+int small_synthesis_end(int dtype, const SynthesisArgs *a, int n);
+cudaError_t launch_synthesis_small(int dtype, const SynthesisArgs *a, int n, cudaStream_t s);
 cudaError_t launch_zero(void *ptr, size_t bytes, cudaStream_t s);
 // FISTA pieces (fista_kernels.cu); n = elements per call (batch * p_alloc for the update)
 // Example 2: batched valid cross-correlation out_b[i] = sum_{j<ta} a_b[j] b_b[i+j]

@@ -295,7 +295,8 @@ def test_native_library_was_used(torch):
     plan = wl.Plan(64, 64, 3, "cdf97", "symmetric", "float32")
     plan.adjoint(torch.randn(64, 64, device="cuda"))
     torch.cuda.synchronize()
-    assert wl.launch_count() - before == 3
+    # one launch per level, or one launch for the small coarse tail (small_kernels.cu)
+    assert 1 <= wl.launch_count() - before <= 3
 
 
 # -------------------------------------------------------------- multi-strip shapes
