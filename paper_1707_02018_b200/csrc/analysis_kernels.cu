@@ -55,6 +55,9 @@ __device__ __forceinline__ int ext_src(int t, int n, int ext, int Lp, T &w) {
   return s;
 }
 
+#ifndef WL_L2HINT
+#define WL_L2HINT 1  // 0: plain stores; 1: LL of a non-last level evict_last; 2: + other subbands evict_first
+#endif
 #ifndef WL_ANA_NS
 #define WL_ANA_NS 2  // A/B on B200: 3 or 4 stages did not beat 2
 #endif
@@ -153,6 +156,7 @@ struct AnaStreamParams {
   P slo[L], shi[L];          // C broadcast taps (f[j], f[j])
   // fused FISTA epilogue (FU): for subbands in fmask the output pointer is y; x = y + xdelta.
   // The W* value g never reaches HBM:  x+ = soft(y - g/L, lambda/L), y+ = x+ + mom (x+ - x)
+  int ll_keep;               // LL feeds the next level: stored evict_last (WL_L2HINT)
   int fmask;
   long long xdelta;
   T inv_lip, tau, mom;
@@ -480,6 +484,15 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
               if (fu1) fista_pair<T, L>(p, mom, d1 + v * pX1, a1[v], ft1 + v * TQ, ft1 + C::FT + v * TQ);
               else *reinterpret_cast<P *>(d1 + v * pX1) = a1[v];
             }
+          } else if (WL_L2HINT && p.ll_keep) {  // LL (setC 0, X = lo) evict_last; the other subbands
+            const uint64_t pol0 = setC == 0 ? l2_evict_last() : l2_evict_first(), pol1 = l2_evict_first();
+#pragma unroll
+            for (int v = 0; v < VC; v++) {
+              if (WL_L2HINT >= 2 || setC == 0) st_hint(reinterpret_cast<P *>(d0 + v * pX0), a0[v], pol0);
+              else *reinterpret_cast<P *>(d0 + v * pX0) = a0[v];
+              if (WL_L2HINT >= 2) st_hint(reinterpret_cast<P *>(d1 + v * pX1), a1[v], pol1);
+              else *reinterpret_cast<P *>(d1 + v * pX1) = a1[v];
+            }
           } else
 #pragma unroll
           for (int v = 0; v < VC; v++) {
@@ -617,6 +630,7 @@ cudaError_t make_ana_params(const AnalysisArgs &a, AnaStreamParams<T, L> &p, boo
     p.slo[j].x = p.slo[j].y = T(a.lo[j]);
     p.shi[j].x = p.shi[j].y = T(a.hi[j]);
   }
+  p.ll_keep = a.ll_keep;
   p.fmask = a.fista_mask;
   p.xdelta = a.fista_xdelta;
   p.inv_lip = T(a.fista_inv_lip);

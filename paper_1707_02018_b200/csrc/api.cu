@@ -214,6 +214,7 @@ wl_status run_analysis(const wl_plan *p, int64_t batch, const void *img, void *x
     a.hi = adjoint ? p->fb.d_hi : p->fb.a_hi;
     a.L = p->fb.L;
     a.batch = (int)batch;
+    a.ll_keep = j < p->J;  // LL_j is read by level j+1 right away
     if (fz) {  // LH/HL/HH of every level and LL of the last land in x
       a.fista_mask = (j == p->J) ? 15 : 14;
       a.fista_xdelta = ((char *)fz->xo - (char *)x) / (int64_t)p->es;
@@ -264,6 +265,7 @@ wl_status run_synthesis(const wl_plan *p, int64_t batch, const void *x, void *im
     a.hi = transpose_of_analysis ? p->fb.a_hi : p->fb.d_hi;
     a.L = p->fb.L;
     a.batch = (int)batch;
+    a.out_keep = j > 1;  // LL_{j-1} is read by level j-1 right away
     int64_t n0 = p->n0[j - 1], n1 = p->n1[j - 1];
     Buf out;
     if (j == 1) {

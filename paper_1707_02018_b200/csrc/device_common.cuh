@@ -183,6 +183,28 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const void *tmap, uint64_
       : "memory");
 }
 
+// L2 eviction-priority policies and stores that carry one (PTX createpolicy / st.L2::cache_hint):
+// a level's LL output is read by the next level right away, so it is stored evict_last; the final
+// coefficients are not re-read by the chain.
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void st_hint(float2 *ptr, float2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;\n" ::"l"(ptr), "f"(v.x), "f"(v.y), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_hint(double2 *ptr, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(ptr), "d"(v.x), "d"(v.y), "l"(pol)
+               : "memory");
+}
+
 // Grid-wide barrier of a cooperative launch (gpu-scope fence included).
 __device__ __forceinline__ void grid_sync_all() { cooperative_groups::this_grid().sync(); }
 // Order this thread's earlier generic-proxy accesses (any state space) before its later

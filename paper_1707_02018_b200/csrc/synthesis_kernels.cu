@@ -37,6 +37,9 @@ namespace {
 
 constexpr int H_MAX = kMaxL / 2;
 
+#ifndef WL_SYN_L2HINT
+#define WL_SYN_L2HINT 1  // the LL outputs of the coarse levels stored evict_last
+#endif
 template <typename T, int L, int NS_ = 0>
 struct SCfg {
   using P = typename Pair<T>::t;
@@ -116,6 +119,7 @@ struct SynStreamParams {
   T *y;                      // split output (symmetric folds): in-image positions go to y
   long long y_pitch, y_bstride;
   int split, yn0, yn1, y_vec;
+  int out_keep;              // the output is the next level's LL: stored evict_last (WL_L2HINT)
   P g1lo[H_MAX], g1hi[H_MAX];  // S1 tap pairs (g[2q+1], g[2q])
   P e_lo[H_MAX], o_lo[H_MAX];  // S0 broadcast taps (g[2q+1], g[2q+1]) and (g[2q], g[2q])
   P e_hi[H_MAX], o_hi[H_MAX];
@@ -321,6 +325,14 @@ __device__ __forceinline__ void syn_level_runs(const SynStreamParams<T, L> &p, u
         } else if ((pair_u || t_hi <= 0 || t_lo >= p.yn0) && vec_ok && run_in && t_lo - p.o0 >= 0 &&
                    t_hi - p.o0 <= p.N0) {
           T *op = out + (long long)(t_lo - p.o0) * p.out_pitch + oc;
+          if (WL_SYN_L2HINT && p.out_keep) {
+            const uint64_t pol = l2_evict_last();
+#pragma unroll
+            for (int v = 0; v < VC; v++) {
+              st_hint(reinterpret_cast<P *>(op + (2 * v) * p.out_pitch), e[v], pol);
+              st_hint(reinterpret_cast<P *>(op + (2 * v + 1) * p.out_pitch), o[v], pol);
+            }
+          } else
 #pragma unroll
           for (int v = 0; v < VC; v++) {
             *reinterpret_cast<P *>(op + (2 * v) * p.out_pitch) = e[v];
@@ -475,6 +487,7 @@ cudaError_t make_syn_params(const SynthesisArgs &a, SynStreamParams<T, L> &p, bo
   p.t01 = 2 * C::VEC * (int)std::floor((double)a.o1 / (2.0 * C::VEC));
   p.vec_store = (a.o1 % 2 == 0) && (a.out_pitch % 2 == 0) && (a.out_bstride % 2 == 0) &&
                 (reinterpret_cast<uintptr_t>(a.out) % (2 * sizeof(T)) == 0);
+  p.out_keep = a.out_keep;
   p.y = static_cast<T *>(a.y);
   p.split = a.y != nullptr;
   p.y_pitch = a.y_pitch;

@@ -41,6 +41,7 @@ struct AnalysisArgs {
   int64_t fista_xdelta = 0;
   double fista_inv_lip = 0, fista_tau = 0, fista_mom = 0;
   const double *fista_tdev = nullptr;  // non-null: the momentum comes from the device-resident t
+  int ll_keep = 0;  // 1: out[0] (LL) is the next level's input: stored with the L2 evict_last policy
 };
 
 struct SynthesisArgs {
@@ -55,6 +56,7 @@ struct SynthesisArgs {
   const double *lo, *hi;
   int L;
   int batch;
+  int out_keep = 0;  // 1: out is the next level's LL input: stored with the L2 evict_last policy
   // split output (symmetric folds): extended positions inside the image, t in [0, yn0) x [0, yn1),
   // go to y (the fold's output, written in place of its interior) and only the rest to out
   void *y = nullptr;
