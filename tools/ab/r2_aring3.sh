@@ -1,5 +1,5 @@
 #!/bin/bash
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 WL_ARING=1 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fista.py -x -q > gpurun_out/par_test.log 2>&1; echo "parity (forced ring) rc=$?"; tail -n 1 gpurun_out/par_test.log
 for A in 1 ""; do echo "== WL_ARING=$A"

@@ -1,6 +1,6 @@
 #!/bin/bash
 # balanced vs banded runs: per-level chain timings (WL_BANDED set = banded)
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 run() {
 timeout 300 python tools/levelbench.py --cfg 4 --ops adjoint,synthesize --reps 20

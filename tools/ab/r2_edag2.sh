@@ -1,5 +1,5 @@
 #!/bin/bash
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fista.py -x -q > gpurun_out/par_test.log 2>&1; echo "parity rc=$?"; tail -n 2 gpurun_out/par_test.log
 timeout 300 python tools/bcbench.py

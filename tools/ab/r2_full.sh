@@ -1,6 +1,6 @@
 #!/bin/bash
 # full GPU check: parity suite, smoke, bench (default), in that order
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 nvidia-smi > gpurun_out/nvidia_smi.txt 2>&1
 lscpu > gpurun_out/lscpu.txt 2>&1

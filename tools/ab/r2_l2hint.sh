@@ -1,5 +1,5 @@
 #!/bin/bash
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/par_test.log 2>&1; echo "parity rc=$?"; tail -n 1 gpurun_out/par_test.log
 for L in "" build/libwl_h0.so build/libwl_h2.so; do echo "== $L"

@@ -1,6 +1,6 @@
 #!/bin/bash
 # launch lists: cfg5 grad step, cfg4 W* chain (with DRAM bytes), cfg5 W / W* chains
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 for spec in "5 grad" "4 adjoint" "5 adjoint" "5 synthesize" "4 synthesize"; do

@@ -1,6 +1,6 @@
 #!/bin/bash
 # round-2 probe: pipe microbench, per-level marginal costs, residual/blur timings
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 tools/microbench/pipes.cu -o /tmp/pipes && timeout 60 /tmp/pipes > gpurun_out/pipes.log 2>&1; echo "pipes rc=$?"
 cat gpurun_out/pipes.log

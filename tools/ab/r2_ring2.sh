@@ -1,5 +1,5 @@
 #!/bin/bash
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 timeout 600 python -m pytest tests/test_gpu_blur_ring.py -x -q > gpurun_out/r2_ring_pytest.log 2>&1; echo "ring pytest rc=$?"; tail -3 gpurun_out/r2_ring_pytest.log
 for op in residual blur grad; do timeout 120 python tools/opbench.py --cfg 5 --op $op --reps 30; done 2>&1 | tee gpurun_out/r2_opbench.log

@@ -1,5 +1,5 @@
 #!/bin/bash
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 for V in "" 1 6 12; do echo "== WL_SHORT_MAX=$V"
 if [ -n "$V" ]; then export WL_SHORT_MAX=$V; else unset WL_SHORT_MAX; fi
 timeout 300 python tools/levelbench.py --cfg 5 --ops adjoint,synthesize --reps 20

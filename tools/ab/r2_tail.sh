@@ -1,5 +1,5 @@
 #!/bin/bash
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_test.log 2>&1; echo "gpu tests rc=$?"; tail -n 3 gpurun_out/gpu_test.log
 for V in "" 1; do echo "== WL_NO_TAIL=$V"
