@@ -35,6 +35,20 @@
 namespace wl {
 namespace {
 
+#ifdef WL_ANA_PROFILE  // debug builds only: per-run start / end times and SM id (tools/anaprof.py)
+__device__ unsigned long long g_ana_prof[8192][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+#endif
+
 // Source index of extended position t (or -1 for a zero) and its weight.
 template <typename T>
 __device__ __forceinline__ int ext_src(int t, int n, int ext, int Lp, T &w) {
@@ -214,6 +228,9 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
   int col, kr0, kr1;
   for (RunIter itr(p.runs); itr.next(col, kr0, kr1);) {
     if (kr0 >= kr1) continue;  // (uniform) empty trailing band
+#ifdef WL_ANA_PROFILE
+    const unsigned long long t_start = gtimer();
+#endif
     const int img = col / p.nstrips, strip = col - img * p.nstrips;
     const int q0 = strip * TQ;
     const int cbox = 2 * q0 + 2 - L - C::SHIFT;  // input column of box column 0 (VEC aligned)
@@ -536,11 +553,26 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
       }
     }
     cp_async_wait_all();
+#ifdef WL_ANA_PROFILE
+    __syncthreads();
+    if (tid == 0 && blockIdx.x < 8192) {
+      g_ana_prof[blockIdx.x][0] = t_start;
+      g_ana_prof[blockIdx.x][1] = gtimer();
+      g_ana_prof[blockIdx.x][2] = smid();
+      g_ana_prof[blockIdx.x][3] = ((unsigned long long)col << 32) | (unsigned)(kr1 - kr0);
+    }
+#endif
   }
 }
 
+#ifndef WL_ANA_REGCAP
+// threads per SM the register allocation must allow (fp32): shared memory holds 4 CTAs of 128 threads, so 512
+// (a 128-register cap; the kernel takes 93).  A/B on B200 against 768 (80 registers): cfg5 W* 167.3 -> 163.4 us,
+// cfg3 W* 101.7 -> 97.1 us, cfg5 grad 558.9 -> 555.1 us; 640: in between
+#define WL_ANA_REGCAP 512
+#endif
 template <typename T, int L, bool FU, int NS, int ZV = 0>
-__global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? 768 / ACfg<T, L, NS, FU>::NT : 1)
+__global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? WL_ANA_REGCAP / ACfg<T, L, NS, FU>::NT : 1)
     k_ana_stream(const __grid_constant__ AnaStreamParams<T, L> p) {
   using C = ACfg<T, L, NS, FU>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -805,6 +837,12 @@ cudaError_t dispatch_chain(const AnalysisArgs *a, int n, cudaStream_t s) {
 }
 
 }  // namespace
+
+#ifdef WL_ANA_PROFILE
+extern "C" __attribute__((visibility("default"))) int wl_debug_ana_prof(void *host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_ana_prof, sizeof(unsigned long long) * 4 * (size_t)n);
+}
+#endif
 
 cudaError_t launch_analysis_chain(int dtype, const AnalysisArgs *a, int n, cudaStream_t s) {
   if (n <= 0 || a[0].batch == 0) return cudaSuccess;

@@ -402,8 +402,11 @@ __device__ __forceinline__ void syn_level_runs(const SynStreamParams<T, L> &p, u
 }
 
 // (the split variant is capped at the plain kernel's register count so it keeps its CTAs per SM)
+#ifndef WL_SYN_REGCAP
+#define WL_SYN_REGCAP 768  // threads per SM the register allocation must allow (fp32)
+#endif
 template <typename T, int L, int NS, int ZV = 0, bool SPLIT = false>
-__global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? (SPLIT ? 1024 : 768) / SCfg<T, L>::NT : 1)
+__global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? (SPLIT ? 1024 : WL_SYN_REGCAP) / SCfg<T, L>::NT : 1)
     k_synth_stream(const __grid_constant__ SynStreamParams<T, L> p) {
   using C = SCfg<T, L, NS>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
