@@ -566,10 +566,11 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
 }
 
 #ifndef WL_ANA_REGCAP
-// threads per SM the register allocation must allow (fp32): shared memory holds 4 CTAs of 128 threads, so 512
-// (a 128-register cap; the kernel takes 93).  A/B on B200 against 768 (80 registers): cfg5 W* 167.3 -> 163.4 us,
-// cfg3 W* 101.7 -> 97.1 us, cfg5 grad 558.9 -> 555.1 us; 640: in between
-#define WL_ANA_REGCAP 512
+// threads per SM the register allocation must allow (fp32).  Shared memory holds 4 CTAs of 128 threads (a
+// 128-register budget); asked for 6 CTAs (768) ptxas stops at 80 registers, for 4 (512) at 93-98, for 3 (384) at
+// 116-124 -- still 4 CTAs per SM, with more loads in flight.  A/B on B200, 768 / 512 / 384: cfg5 W* 167.3 / 163.4 /
+// 161.4 us, cfg3 W* 101.7 / 97.1 / 96.0 us, cfg5 grad 558.9 / 555.1 / 549.2 us (with the ring blur's cap)
+#define WL_ANA_REGCAP 384
 #endif
 template <typename T, int L, bool FU, int NS, int ZV = 0>
 __global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? WL_ANA_REGCAP / ACfg<T, L, NS, FU>::NT : 1)

@@ -169,11 +169,14 @@ __device__ __forceinline__ float2 vring(const float2 (&ring)[kRing], int nw, con
   return a;
 }
 
+// Register cap: shared memory holds 4 CTAs of 128 threads, i.e. 128 registers.  Asking ptxas for 4 CTAs makes it
+// stop at 106 registers; asking for 3 lets the long PSFs (half-width >= 5) take 121-126, still 4 CTAs per SM:
+// cfg5 residual 251.6 -> 247.4 us, grad 555.9 -> 551.3 us.  The shorter PSFs would pass 128 (3 CTAs) and keep 4.
 #ifndef WL_RING_MINB
-#define WL_RING_MINB (8 / WL_RING_NB)
+#define WL_RING_MINB(HW) ((HW) >= 5 ? 6 / WL_RING_NB : 8 / WL_RING_NB)
 #endif
 template <int HW, bool RESID>
-__global__ void __launch_bounds__(64 * WL_RING_NB, WL_RING_MINB) k_blur_ring(const __grid_constant__ RingParams<HW> p) {
+__global__ void __launch_bounds__(64 * WL_RING_NB, WL_RING_MINB(HW)) k_blur_ring(const __grid_constant__ RingParams<HW> p) {
   using C = RingCfg<HW, RESID>;
   constexpr int G = C::G, S = C::S, NWIN = C::NWIN, S0 = C::S0;
   extern __shared__ __align__(128) unsigned char sm[];
