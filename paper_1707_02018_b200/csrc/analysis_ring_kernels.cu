@@ -47,7 +47,7 @@ struct ARingCfg {
   static constexpr int NSG = (L / 2 >= 4) ? L / 2 : 4;  // steps per group: whole ring periods (L/2)
   static constexpr int G = 2 * NSG;                     // input rows per group
 #ifndef WL_ARING_S
-#define WL_ARING_S 3
+#define WL_ARING_S 2  // A/B on B200: 2 stages (5 CTAs per SM, register-bound) beat 3 (4 CTAs): cfg4 W* level 1 38.9 -> 36.9 us cold
 #endif
   static constexpr int S = WL_ARING_S;                  // shared-memory stages
   static constexpr int REG = round_up_c(G * UBX * 4, 128) / 4;  // floats per (stage, box)
