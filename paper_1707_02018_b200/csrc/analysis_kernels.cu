@@ -202,7 +202,10 @@ __device__ __forceinline__ void fista_pair(const AnaStreamParams<T, L> &p, T mom
 
 // One level's runs, handed to the CTAs of the grid (the body of k_ana_stream; k_ana_multi calls it
 // once per level of the coarse tail).  `phase` carries the stage barriers' parities across calls.
-template <typename T, int L, bool FU, int NS, int ZV = 0>
+// PLAIN: zero extension with every block by TMA (W* under zero / symmetric BC on 16-byte aligned input): the gather,
+// bulk-row, wrap and mirror paths are compiled out (a compact hot path: the coarse levels start with a cold
+// instruction cache).
+template <typename T, int L, bool FU, int NS, int ZV = 0, bool PLAIN = false>
 __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, unsigned char *smem_raw,
                                                unsigned &phase) {
   using C = ACfg<T, L, NS, FU>;
@@ -241,7 +244,7 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
     // their mirror images inside the box
     const int fix_lim = min(cbox + C::UW, 2 * p.m1);
     const int fix_nl = max(0, min(-cbox, C::UW)), fix_r0 = max(p.n1, cbox), fix_nr = max(0, fix_lim - fix_r0);
-    const bool sym_fix = (p.ext == EXT_SYM || p.ext == EXT_SYM_PADJ) && !cols_in &&
+    const bool sym_fix = !PLAIN && (p.ext == EXT_SYM || p.ext == EXT_SYM_PADJ) && !cols_in &&
                          (cbox >= 0 || -2 * cbox - 1 < C::UW) && (fix_nr == 0 || 2 * p.n1 - fix_lim >= cbox);
     const int nblk = (kr1 - kr0 + G - 1) / G;
     // C output columns q = q0 + 2 mC (+1) of subbands (setC: LL/HL from lo, LH/HH from hi)
@@ -267,6 +270,14 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
                          (arr ? p.xdelta : 0);
           cp_async16(fdst + ((band * 2 + arr) * G + r) * TQ + c * VEC, src);
         }
+      }
+      if (PLAIN) {  // TMA's zero fill is the zero extension
+        if (tid == 0) {
+          fence_proxy_async();
+          mbar_arrive_expect_tx(bar + sl, GI * C::UW * sizeof(T));
+          tma_load_3d(dst0, &p.tmap, bar + sl, cbox, r_in, img);
+        }
+        return true;
       }
       // (E_sym^dagger)*: TMA only where every row and column weight is 1 (L-1 inside the edges)
       const int wpad = p.ext == EXT_SYM_PADJ ? L - 1 : 0;
@@ -365,7 +376,9 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
 
     __syncthreads();  // previous run's readers are done
     unsigned armed = 0;  // bit s: the batch in slot s armed its barrier
-#pragma unroll
+    // (a loop, not NS-1 inlined copies of the block loader: the short-run variant's code 98 -> 59 KB and the coarse
+    // levels, which start with a cold instruction cache, run faster: cfg5 W* 156.6 -> 153.0 us, cfg3 92.2 -> 88.7 us)
+#pragma unroll 1
     for (int b = -1; b < C::NS - 2; b++) {
       if (b < nblk && load_block(b)) armed |= 1u << ((b + 1) % C::NS);
       cp_async_commit();
@@ -373,7 +386,7 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
     for (int it = -1; it < nblk; it++) {
       const int slot = (it + 1) % C::NS;
       cp_async_wait_group<C::NS - 2>();  // this thread's gathers of block it are done
-      const bool async_blk = (armed >> slot) & 1;  // block it came by TMA / bulk copies
+      const bool async_blk = PLAIN || ((armed >> slot) & 1);  // block it came by TMA / bulk copies
       if (async_blk) {
         mbar_wait(bar + slot, (phase >> slot) & 1);
         phase ^= 1u << slot;
@@ -381,7 +394,7 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
       __syncthreads();  // (1) block it landed; the history move of it-1 is done
       bool padj_rows = false;  // async (E_sym^dagger)* block with weighted rows
       const int r_blk = 2 * (kr0 + it * G);
-      if (async_blk && (p.ext == EXT_SYM || p.ext == EXT_SYM_PADJ)) {
+      if (!PLAIN && async_blk && (p.ext == EXT_SYM || p.ext == EXT_SYM_PADJ)) {
         const int wpad = p.ext == EXT_SYM_PADJ ? L - 1 : 0;
         const bool blk_rows_in = r_blk >= wpad && r_blk + GI <= p.n0 - wpad;
         T *ub = ubuf + slot * GI * C::UP;
@@ -439,7 +452,7 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
 #pragma unroll
           for (int k = 0; k < V; k++) acc[k] = fma2(f, splat2<P>(win[C::SHIFT + 2 * k + L - 1 - j]), acc[k]);
         }
-        if (padj_rows) {  // (E_sym^dagger)* row weight 1/c of the row's source (linear: scale the output)
+        if (!PLAIN && padj_rows) {  // (E_sym^dagger)* row weight 1/c of the row's source (linear: scale the output)
           const int sr = refl_inf(r_blk + rowB, p.n0), Lp = L - 1;
           const int c = 1 + (sr < Lp ? 1 : 0) + (sr >= p.n0 - Lp ? 1 : 0);
           if (c > 1) {
@@ -572,7 +585,7 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
 // 161.4 us, cfg3 W* 101.7 / 97.1 / 96.0 us, cfg5 grad 558.9 / 555.1 / 549.2 us (with the ring blur's cap)
 #define WL_ANA_REGCAP 384
 #endif
-template <typename T, int L, bool FU, int NS, int ZV = 0>
+template <typename T, int L, bool FU, int NS, int ZV = 0, bool PLAIN = false>
 __global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? WL_ANA_REGCAP / ACfg<T, L, NS, FU>::NT : 1)
     k_ana_stream(const __grid_constant__ AnaStreamParams<T, L> p) {
   using C = ACfg<T, L, NS, FU>;
@@ -585,7 +598,7 @@ __global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? WL_AN
   pdl_launch_dependents();
   pdl_wait();  // the previous kernel of the stream wrote our inputs
   unsigned phase = 0;
-  ana_level_runs<T, L, FU, NS, ZV>(p, smem_raw, phase);
+  ana_level_runs<T, L, FU, NS, ZV, PLAIN>(p, smem_raw, phase);
 }
 
 // The coarse tail of a W* / W-dagger chain in one persistent launch: levels
@@ -713,18 +726,21 @@ cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
   cudaError_t e = make_ana_params<T, L, FU>(a, p, short_run, false);
   if (e != cudaSuccess) return e;
   long long resident = 0;
+  // the compact zero-extension instantiation (fp32, plain stores) when every block comes by TMA
+  constexpr bool HAS_PLAIN = !FU && sizeof(T) == 4;
+  const bool plain = HAS_PLAIN && p.tma && p.tma_any_block && plain_enabled();
+  auto kshort = plain ? k_ana_stream<T, L, FU, 4, ZV, HAS_PLAIN> : k_ana_stream<T, L, FU, 4, ZV, false>;
+  auto klong = plain ? k_ana_stream<T, L, FU, 0, ZV, HAS_PLAIN> : k_ana_stream<T, L, FU, 0, ZV, false>;
   if (short_run) {
-    e = kernel_resident(reinterpret_cast<const void *>(k_ana_stream<T, L, FU, 4, ZV>), C4::NT, C4::smem_bytes(FU),
-                        &resident);
+    e = kernel_resident(reinterpret_cast<const void *>(kshort), C4::NT, C4::smem_bytes(FU), &resident);
     if (e != cudaSuccess) return e;
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
-    e = launch_pdl(k_ana_stream<T, L, FU, 4, ZV>, grid, C4::NT, C4::smem_bytes(FU), s, p, 'a');
+    e = launch_pdl(kshort, grid, C4::NT, C4::smem_bytes(FU), s, p, 'a');
   } else {
-    e = kernel_resident(reinterpret_cast<const void *>(k_ana_stream<T, L, FU, 0, ZV>), C::NT, C::smem_bytes(FU),
-                        &resident);
+    e = kernel_resident(reinterpret_cast<const void *>(klong), C::NT, C::smem_bytes(FU), &resident);
     if (e != cudaSuccess) return e;
     const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
-    e = launch_pdl(k_ana_stream<T, L, FU, 0, ZV>, grid, C::NT, C::smem_bytes(FU), s, p, 'A');
+    e = launch_pdl(klong, grid, C::NT, C::smem_bytes(FU), s, p, 'A');
   }
   g_launches++;
   if (e != cudaSuccess) return e;

@@ -223,7 +223,7 @@ __device__ __forceinline__ void syn_level_runs(const SynStreamParams<T, L> &p, u
 
     __syncthreads();  // previous run's readers are done
     unsigned armed = 0;  // bit s: the batch in slot s armed its barrier
-#pragma unroll
+#pragma unroll 1  // one copy of the batch loader (code size; see the analysis kernel)
     for (int k = 0; k < C::NS - 1; k++) {
       if (k < n_it && load_batch(k)) armed |= 1u << (k % C::NS);
       cp_async_commit();

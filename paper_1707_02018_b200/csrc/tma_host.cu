@@ -104,6 +104,11 @@ bool balanced_runs() {
   return v;
 }
 
+bool plain_enabled() {
+  static const bool v = getenv("WL_NO_PLAIN") == nullptr;
+  return v;
+}
+
 bool multi_enabled() {
   // measured on B200 (graph replay): the cooperative multi-level tail lost to per-level PDL
   // launches (cfg4 W* 96 vs 80 us, cfg2 W* 26 vs 17 us): off unless WL_MULTI is set
