@@ -127,7 +127,9 @@ struct SynStreamParams {
 
 // One level's runs (the body of k_synth_stream; k_synth_multi calls it once per level of the
 // coarse head of a W chain).  `phase` carries the stage barriers' parities across calls.
-template <typename T, int L, int NS, int ZV = 0, bool SPLIT = false>
+// PLAIN: crop (zero coefficients outside) with every window by TMA: the gather path is compiled out (a compact hot
+// path for the coarse levels, which start with a cold instruction cache; see the analysis kernel).
+template <typename T, int L, int NS, int ZV = 0, bool SPLIT = false, bool PLAIN = false>
 __device__ __forceinline__ void syn_level_runs(const SynStreamParams<T, L> &p, unsigned char *smem_raw,
                                                unsigned &phase) {
   using C = SCfg<T, L, NS>;
@@ -169,7 +171,7 @@ __device__ __forceinline__ void syn_level_runs(const SynStreamParams<T, L> &p, u
       const int sl = k % C::NS;
       T *dst0 = cbuf + sl * 4 * C::BAND_ELEMS;
       // periodic plans: TMA only for windows that need no wrap (the zero fill is the crop otherwise)
-      if (p.tma && (!p.coef_mod || (kr >= 0 && kr + G <= p.m0 && kc0 >= 0 && kc0 + C::KCW <= p.m1))) {
+      if (PLAIN || (p.tma && (!p.coef_mod || (kr >= 0 && kr + G <= p.m0 && kc0 >= 0 && kc0 + C::KCW <= p.m1)))) {
         if (tid == 0) {
           fence_proxy_async();
           mbar_arrive_expect_tx(bar + sl, 4 * C::BAND_ELEMS * sizeof(T));
@@ -178,6 +180,7 @@ __device__ __forceinline__ void syn_level_runs(const SynStreamParams<T, L> &p, u
         }
         return true;
       }
+      if (PLAIN) return true;  // (unreachable: the branch above is taken)
       for (int idx = tid; idx < 4 * G * C::NCH; idx += C::NT) {
         const int bnd = idx / (G * C::NCH), rem = idx - bnd * G * C::NCH;
         const int r = rem / C::NCH, v = rem - r * C::NCH;
@@ -405,7 +408,7 @@ __device__ __forceinline__ void syn_level_runs(const SynStreamParams<T, L> &p, u
 #ifndef WL_SYN_REGCAP
 #define WL_SYN_REGCAP 768  // threads per SM the register allocation must allow (fp32)
 #endif
-template <typename T, int L, int NS, int ZV = 0, bool SPLIT = false>
+template <typename T, int L, int NS, int ZV = 0, bool SPLIT = false, bool PLAIN = false>
 __global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? (SPLIT ? 1024 : WL_SYN_REGCAP) / SCfg<T, L>::NT : 1)
     k_synth_stream(const __grid_constant__ SynStreamParams<T, L> p) {
   using C = SCfg<T, L, NS>;
@@ -418,7 +421,7 @@ __global__ void __launch_bounds__(SCfg<T, L>::NT, sizeof(T) == 4 ? (SPLIT ? 1024
   pdl_launch_dependents();
   pdl_wait();  // the previous kernel of the stream wrote our inputs
   unsigned phase = 0;
-  syn_level_runs<T, L, NS, ZV, SPLIT>(p, smem_raw, phase);
+  syn_level_runs<T, L, NS, ZV, SPLIT, PLAIN>(p, smem_raw, phase);
 }
 
 // The coarse head of a W chain (levels J .. j0, coarse -> fine) in one persistent cooperative
@@ -548,8 +551,13 @@ cudaError_t launch_synth_stream_t(const SynthesisArgs &a, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   long long resident = 0;
   // split outputs (symmetric folds) take their own instantiation: the routing costs registers
-  auto kshort = p.split ? k_synth_stream<T, L, 4, ZV, true> : k_synth_stream<T, L, 4, ZV, false>;
-  auto klong = p.split ? k_synth_stream<T, L, 0, ZV, true> : k_synth_stream<T, L, 0, ZV, false>;
+  // the compact crop instantiation (fp32) when every window comes by TMA
+  constexpr bool HAS_PLAIN = sizeof(T) == 4;
+  const bool plain = HAS_PLAIN && !p.split && p.tma && !p.coef_mod && plain_enabled();
+  auto kshort = p.split ? k_synth_stream<T, L, 4, ZV, true>
+                        : (plain ? k_synth_stream<T, L, 4, ZV, false, HAS_PLAIN> : k_synth_stream<T, L, 4, ZV, false>);
+  auto klong = p.split ? k_synth_stream<T, L, 0, ZV, true>
+                       : (plain ? k_synth_stream<T, L, 0, ZV, false, HAS_PLAIN> : k_synth_stream<T, L, 0, ZV, false>);
   if (short_run) {
     e = kernel_resident(reinterpret_cast<const void *>(kshort), C4::NT, C4::smem_bytes(), &resident);
     if (e != cudaSuccess) return e;

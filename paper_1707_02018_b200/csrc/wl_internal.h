@@ -186,7 +186,8 @@ bool multi_enabled();
 // balanced (equal-row, column-spanning) runs for the analysis / synthesis level kernels (A/B: WL_BALANCED=1;
 // measured slower, see RunMap)
 bool balanced_runs();
-// the compact zero-extension instantiation of the analysis level kernel unless WL_NO_PLAIN is set (A/B switch)
+// the compact instantiations of the level kernels (analysis: zero extension, synthesis: crop; every block by
+// TMA) unless WL_NO_PLAIN is set (A/B switch)
 bool plain_enabled();
 
 // PDL per launch site: kind 'A' / 'a' (analysis, long / short runs), 'S' / 's' (synthesis), 'b'
