@@ -727,7 +727,7 @@ cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   long long resident = 0;
   // the compact zero-extension instantiation (fp32, plain stores) when every block comes by TMA
-  constexpr bool HAS_PLAIN = !FU && sizeof(T) == 4;
+  constexpr bool HAS_PLAIN = sizeof(T) == 4;
   const bool plain = HAS_PLAIN && p.tma && p.tma_any_block && plain_enabled();
   auto kshort = plain ? k_ana_stream<T, L, FU, 4, ZV, HAS_PLAIN> : k_ana_stream<T, L, FU, 4, ZV, false>;
   auto klong = plain ? k_ana_stream<T, L, FU, 0, ZV, HAS_PLAIN> : k_ana_stream<T, L, FU, 0, ZV, false>;
