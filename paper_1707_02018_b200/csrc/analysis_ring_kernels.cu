@@ -242,7 +242,11 @@ bool launch_analysis_ring(int dtype, const AnalysisArgs &a, cudaStream_t s, cuda
   // and on small levels (short bands: the L - 2 priming rows per band dominate).  WL_ARING=1 forces
   // it for every zero-extension level (A/B).
   static const bool force = getenv("WL_ARING") != nullptr;
-  if (!force && (a.L < 16 || (long long)a.batch * a.m0 * a.m1 < (1LL << 20))) return false;
+  static const int min_log2 = [] {
+    const char *e = getenv("WL_ARING_MIN");  // A/B: log2 of the smallest level (in coefficients) the ring takes
+    return e ? atoi(e) : 20;
+  }();
+  if (!force && (a.L < 16 || (long long)a.batch * a.m0 * a.m1 < (1LL << min_log2))) return false;
   // one pitch for the four subbands, 16-byte aligned rows and images (TMA strides), aligned base
   for (int i = 1; i < 4; i++)
     if (a.out_pitch[i] != a.out_pitch[0]) return false;

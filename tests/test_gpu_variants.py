@@ -1,7 +1,8 @@
 """The operator parity tests re-run in child processes under the library's path switches (each is read once
 per process, so a child is the only way to flip it): the small-level kernels off (WL_NO_SMALL: the streaming
 kernels then take the small shapes too), the register-ring analysis forced onto every zero-extension level
-(WL_ARING), and the full-frame symmetric fold (WL_FULL_FOLD).  Every variant must stay within the same oracle
+(WL_ARING), the full-frame symmetric fold (WL_FULL_FOLD), and the general level kernels in place of the compact
+zero-extension / crop instantiations (WL_NO_PLAIN).  Every variant must stay within the same oracle
 tolerances, so no code path the defaults do not take goes untested.
 """
 import os
@@ -23,7 +24,7 @@ def torch():
     return torch
 
 
-@pytest.mark.parametrize("env", ["WL_NO_SMALL", "WL_ARING", "WL_FULL_FOLD"])
+@pytest.mark.parametrize("env", ["WL_NO_SMALL", "WL_ARING", "WL_FULL_FOLD", "WL_NO_PLAIN"])
 def test_operator_parity_under_switch(torch, env):
     e = dict(os.environ)
     e[env] = "1"
