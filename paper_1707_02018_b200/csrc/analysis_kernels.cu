@@ -200,6 +200,46 @@ __device__ __forceinline__ void fista_pair(const AnaStreamParams<T, L> &p, T mom
   *reinterpret_cast<P *>(yp) = yn;
 }
 
+// The element-gather load of one input block (any extension, any alignment): the fallback of the block loader,
+// kept out of line so the kernel's hot paths stay compact (instruction-cache footprint).
+template <typename T, int L, typename C>
+__device__ __noinline__ void gather_block(const AnaStreamParams<T, L> &p, const T *in, T *dst0, int r_in, int cbox,
+                                          int tid) {
+  using Vt = typename Vec16<T>::type;
+  constexpr int GI = C::GI, VEC = C::VEC;
+  for (int idx = tid; idx < GI * C::NV; idx += C::NT) {
+    const int r = idx / C::NV, v = idx - r * C::NV;
+    T wr;
+    const int sr = ext_src<T>(r_in + r, p.n0, p.ext, L - 1, wr);
+    T *dst = dst0 + r * C::UP + v * VEC;
+    const int cg = cbox + v * VEC;
+    // extended positions t >= 2m feed no stored output (out[k] reads t = 2k+1-j <= 2m-1): the
+    // window of a partial last strip / band is zero-filled there instead of gathered
+    if (sr < 0 || cg >= 2 * p.m1 || r_in + r >= 2 * p.m0) {
+      T z[VEC];
+#pragma unroll
+      for (int u = 0; u < VEC; u++) z[u] = T(0);
+      *reinterpret_cast<Vt *>(dst) = vec_make<T>(z);
+    } else if (p.fast && cg >= 0 && cg + VEC <= p.n1 &&
+               (p.ext != EXT_SYM_PADJ || (wr == T(1) && cg >= L - 1 && cg + VEC <= p.n1 - (L - 1)))) {
+      // a plain 16-byte copy (for the weighted (E_sym^dagger)* extension only where every weight is 1)
+      cp_async16(dst, in + (long long)sr * p.in_pitch + cg);
+    } else if (p.fast && p.ext == EXT_PER && p.n1 % VEC == 0 && ((cg % p.n1) + p.n1) % p.n1 + VEC <= p.n1) {
+      // periodic wrap of a whole aligned chunk (n1 is a multiple of VEC when p.fast)
+      cp_async16(dst, in + (long long)sr * p.in_pitch + ((cg % p.n1) + p.n1) % p.n1);
+    } else {
+      T z[VEC];
+#pragma unroll
+      for (int u = 0; u < VEC; u++) {
+        T wc;
+        const int sc = ext_src<T>(cg + u, p.n1, p.ext, L - 1, wc);
+        z[u] = sc >= 0 ? in[(long long)sr * p.in_pitch + sc] * (wr * wc) : T(0);
+      }
+      *reinterpret_cast<Vt *>(dst) = vec_make<T>(z);
+    }
+  }
+}
+
 // One level's runs, handed to the CTAs of the grid (the body of k_ana_stream; k_ana_multi calls it
 // once per level of the coarse tail).  `phase` carries the stage barriers' parities across calls.
 // PLAIN: zero extension with every block by TMA (W* under zero / symmetric BC on 16-byte aligned input): the gather,
@@ -340,37 +380,7 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
         }
         return true;
       }
-      for (int idx = tid; idx < GI * C::NV; idx += C::NT) {
-        const int r = idx / C::NV, v = idx - r * C::NV;
-        T wr;
-        const int sr = ext_src<T>(r_in + r, p.n0, p.ext, L - 1, wr);
-        T *dst = dst0 + r * C::UP + v * VEC;
-        const int cg = cbox + v * VEC;
-        // extended positions t >= 2m feed no stored output (out[k] reads t = 2k+1-j <= 2m-1): the
-        // window of a partial last strip / band is zero-filled there instead of gathered
-        if (sr < 0 || cg >= 2 * p.m1 || r_in + r >= 2 * p.m0) {
-          T z[VEC];
-#pragma unroll
-          for (int u = 0; u < VEC; u++) z[u] = T(0);
-          *reinterpret_cast<Vt *>(dst) = vec_make<T>(z);
-        } else if (p.fast && cg >= 0 && cg + VEC <= p.n1 &&
-                   (p.ext != EXT_SYM_PADJ || (wr == T(1) && cg >= L - 1 && cg + VEC <= p.n1 - (L - 1)))) {
-          // a plain 16-byte copy (for the weighted (E_sym^dagger)* extension only where every weight is 1)
-          cp_async16(dst, in + (long long)sr * p.in_pitch + cg);
-        } else if (p.fast && p.ext == EXT_PER && p.n1 % VEC == 0 && ((cg % p.n1) + p.n1) % p.n1 + VEC <= p.n1) {
-          // periodic wrap of a whole aligned chunk (n1 is a multiple of VEC when p.fast)
-          cp_async16(dst, in + (long long)sr * p.in_pitch + ((cg % p.n1) + p.n1) % p.n1);
-        } else {
-          T z[VEC];
-#pragma unroll
-          for (int u = 0; u < VEC; u++) {
-            T wc;
-            const int sc = ext_src<T>(cg + u, p.n1, p.ext, L - 1, wc);
-            z[u] = sc >= 0 ? in[(long long)sr * p.in_pitch + sc] * (wr * wc) : T(0);
-          }
-          *reinterpret_cast<Vt *>(dst) = vec_make<T>(z);
-        }
-      }
+      gather_block<T, L, C>(p, in, dst0, r_in, cbox, tid);
       return false;
     };
 
