@@ -204,13 +204,13 @@ __device__ __forceinline__ void fista_pair(const AnaStreamParams<T, L> &p, T mom
 // kept out of line so the kernel's hot paths stay compact (instruction-cache footprint).
 template <typename T, int L, typename C>
 __device__ __noinline__ void gather_block(const AnaStreamParams<T, L> &p, const T *in, T *dst0, int r_in, int cbox,
-                                          int tid) {
+                                          int tid, int ext) {
   using Vt = typename Vec16<T>::type;
   constexpr int GI = C::GI, VEC = C::VEC;
   for (int idx = tid; idx < GI * C::NV; idx += C::NT) {
     const int r = idx / C::NV, v = idx - r * C::NV;
     T wr;
-    const int sr = ext_src<T>(r_in + r, p.n0, p.ext, L - 1, wr);
+    const int sr = ext_src<T>(r_in + r, p.n0, ext, L - 1, wr);
     T *dst = dst0 + r * C::UP + v * VEC;
     const int cg = cbox + v * VEC;
     // extended positions t >= 2m feed no stored output (out[k] reads t = 2k+1-j <= 2m-1): the
@@ -221,10 +221,10 @@ __device__ __noinline__ void gather_block(const AnaStreamParams<T, L> &p, const 
       for (int u = 0; u < VEC; u++) z[u] = T(0);
       *reinterpret_cast<Vt *>(dst) = vec_make<T>(z);
     } else if (p.fast && cg >= 0 && cg + VEC <= p.n1 &&
-               (p.ext != EXT_SYM_PADJ || (wr == T(1) && cg >= L - 1 && cg + VEC <= p.n1 - (L - 1)))) {
+               (ext != EXT_SYM_PADJ || (wr == T(1) && cg >= L - 1 && cg + VEC <= p.n1 - (L - 1)))) {
       // a plain 16-byte copy (for the weighted (E_sym^dagger)* extension only where every weight is 1)
       cp_async16(dst, in + (long long)sr * p.in_pitch + cg);
-    } else if (p.fast && p.ext == EXT_PER && p.n1 % VEC == 0 && ((cg % p.n1) + p.n1) % p.n1 + VEC <= p.n1) {
+    } else if (p.fast && ext == EXT_PER && p.n1 % VEC == 0 && ((cg % p.n1) + p.n1) % p.n1 + VEC <= p.n1) {
       // periodic wrap of a whole aligned chunk (n1 is a multiple of VEC when p.fast)
       cp_async16(dst, in + (long long)sr * p.in_pitch + ((cg % p.n1) + p.n1) % p.n1);
     } else {
@@ -232,7 +232,7 @@ __device__ __noinline__ void gather_block(const AnaStreamParams<T, L> &p, const 
 #pragma unroll
       for (int u = 0; u < VEC; u++) {
         T wc;
-        const int sc = ext_src<T>(cg + u, p.n1, p.ext, L - 1, wc);
+        const int sc = ext_src<T>(cg + u, p.n1, ext, L - 1, wc);
         z[u] = sc >= 0 ? in[(long long)sr * p.in_pitch + sc] * (wr * wc) : T(0);
       }
       *reinterpret_cast<Vt *>(dst) = vec_make<T>(z);
@@ -242,12 +242,15 @@ __device__ __noinline__ void gather_block(const AnaStreamParams<T, L> &p, const 
 
 // One level's runs, handed to the CTAs of the grid (the body of k_ana_stream; k_ana_multi calls it
 // once per level of the coarse tail).  `phase` carries the stage barriers' parities across calls.
-// PLAIN: zero extension with every block by TMA (W* under zero / symmetric BC on 16-byte aligned input): the gather,
-// bulk-row, wrap and mirror paths are compiled out (a compact hot path: the coarse levels start with a cold
-// instruction cache).
-template <typename T, int L, bool FU, int NS, int ZV = 0, bool PLAIN = false>
+// KIND 1 (PLAIN): zero extension with every block by TMA (W* under zero / symmetric BC on 16-byte aligned input): the
+// gather, bulk-row, wrap and mirror paths are compiled out (a compact hot path: the coarse levels start with a cold
+// instruction cache).  KIND 2 / 3: the extension is E_sym / (E_sym^dagger)* at compile time (W-dagger under symmetric
+// BC, the paper-literal W*): the wrap path and the other extension's branches are compiled out.  KIND 0: p.ext.
+template <typename T, int L, bool FU, int NS, int ZV = 0, int KIND = 0>
 __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, unsigned char *smem_raw,
                                                unsigned &phase) {
+  constexpr bool PLAIN = KIND == 1;
+  const int ext = KIND == 1 ? EXT_ZERO : (KIND == 2 ? EXT_SYM : (KIND == 3 ? EXT_SYM_PADJ : p.ext));
   using C = ACfg<T, L, NS, FU>;
   using P = typename C::P;
   using Vt = typename Vec16<T>::type;
@@ -278,13 +281,13 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
     const int q0 = strip * TQ;
     const int cbox = 2 * q0 + 2 - L - C::SHIFT;  // input column of box column 0 (VEC aligned)
     const T *in = p.in + (long long)img * p.in_bstride;
-    const int wpc = p.ext == EXT_SYM_PADJ ? L - 1 : 0;  // weighted edge columns (E_sym^dagger)*
+    const int wpc = ext == EXT_SYM_PADJ ? L - 1 : 0;  // weighted edge columns (E_sym^dagger)*
     const bool cols_in = cbox >= wpc && cbox + C::UW <= p.n1 - wpc;
     // outside columns a stored output reads: [cbox, 0) and [n1, min(cbox + UW, 2 m1)); sym_fix needs
     // their mirror images inside the box
     const int fix_lim = min(cbox + C::UW, 2 * p.m1);
     const int fix_nl = max(0, min(-cbox, C::UW)), fix_r0 = max(p.n1, cbox), fix_nr = max(0, fix_lim - fix_r0);
-    const bool sym_fix = !PLAIN && (p.ext == EXT_SYM || p.ext == EXT_SYM_PADJ) && !cols_in &&
+    const bool sym_fix = !PLAIN && (ext == EXT_SYM || ext == EXT_SYM_PADJ) && !cols_in &&
                          (cbox >= 0 || -2 * cbox - 1 < C::UW) && (fix_nr == 0 || 2 * p.n1 - fix_lim >= cbox);
     const int nblk = (kr1 - kr0 + G - 1) / G;
     // C output columns q = q0 + 2 mC (+1) of subbands (setC: LL/HL from lo, LH/HH from hi)
@@ -320,7 +323,7 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
         return true;
       }
       // (E_sym^dagger)*: TMA only where every row and column weight is 1 (L-1 inside the edges)
-      const int wpad = p.ext == EXT_SYM_PADJ ? L - 1 : 0;
+      const int wpad = ext == EXT_SYM_PADJ ? L - 1 : 0;
       const bool rows_in = r_in >= wpad && r_in + GI <= p.n0 - wpad;
       // symmetric edge strips: the box still comes by TMA (zero fill outside) and the outside
       // columns are mirrored inside shared memory after it lands (sym_fix)
@@ -338,7 +341,7 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
       // are mirrored and the (E_sym^dagger)* column weights applied in shared memory after it
       // lands, the row weights to the B-stage output.  (TMA row boxes would need 128-byte aligned
       // shared rows.)
-      if (p.tma && (p.ext == EXT_SYM || p.ext == EXT_SYM_PADJ) && (cols_in || sym_fix)) {
+      if (p.tma && (ext == EXT_SYM || ext == EXT_SYM_PADJ) && (cols_in || sym_fix)) {
         if (tid < 32) {  // warp 0: lane r copies rows r, r + 32, ...
           const int a0 = max(cbox, 0), e = min(cbox + C::UW, p.n1), e4 = max(a0, e / VEC * VEC);
           if (tid == 0) mbar_arrive_expect_tx(bar + sl, (unsigned)(GI * (e4 - a0) * sizeof(T)));
@@ -357,7 +360,7 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
       // in-image columns (warp 0's lanes) and cp.async of the wrapped 16-byte chunks at either end (all
       // threads), from the wrapped source row (reading R2: indices mod n) -- every box column
       // filled, no shared-memory fix
-      if (p.tma && p.ext == EXT_PER && p.n1 % VEC == 0 && -cbox <= p.n1 && cbox + C::UW - p.n1 <= p.n1) {
+      if (p.tma && ext == EXT_PER && p.n1 % VEC == 0 && -cbox <= p.n1 && cbox + C::UW - p.n1 <= p.n1) {
         const int a0 = max(cbox, 0), e = min(cbox + C::UW, p.n1);
         const int nl = max(0, -cbox) / VEC, nr = max(0, cbox + C::UW - p.n1) / VEC;  // wrapped chunks
         auto row_of = [&](int r) {
@@ -380,7 +383,7 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
         }
         return true;
       }
-      gather_block<T, L, C>(p, in, dst0, r_in, cbox, tid);
+      gather_block<T, L, C>(p, in, dst0, r_in, cbox, tid, ext);
       return false;
     };
 
@@ -404,8 +407,8 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
       __syncthreads();  // (1) block it landed; the history move of it-1 is done
       bool padj_rows = false;  // async (E_sym^dagger)* block with weighted rows
       const int r_blk = 2 * (kr0 + it * G);
-      if (!PLAIN && async_blk && (p.ext == EXT_SYM || p.ext == EXT_SYM_PADJ)) {
-        const int wpad = p.ext == EXT_SYM_PADJ ? L - 1 : 0;
+      if (!PLAIN && async_blk && (ext == EXT_SYM || ext == EXT_SYM_PADJ)) {
+        const int wpad = ext == EXT_SYM_PADJ ? L - 1 : 0;
         const bool blk_rows_in = r_blk >= wpad && r_blk + GI <= p.n0 - wpad;
         T *ub = ubuf + slot * GI * C::UP;
         if (sym_fix) {
@@ -413,7 +416,7 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
           // mirror images [cbox, 0) / [n1, fix_lim) (half-point reflection) and, for
           // (E_sym^dagger)* = E_sym diag(1/c), scales s and its images by 1/c_s
           // (c = 1 + [s < L-1] + [s >= n-L+1]).  Reading each source once keeps it race-free.
-          const int Lw = p.ext == EXT_SYM_PADJ ? L - 1 : 0;
+          const int Lw = ext == EXT_SYM_PADJ ? L - 1 : 0;
           const int a = min(max(Lw, fix_nl), p.n1);              // left sources [0, a)
           const int b0 = max(a, p.n1 - max(Lw, fix_nr));          // right sources [b0, n1)
           const int la0 = max(0, cbox), la1 = min(a, cbox + C::UW);
@@ -437,7 +440,7 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
           __syncthreads();
         }
         // rows of (E_sym^dagger)*: applied to the B-stage output of the row (row_w below)
-        padj_rows = p.ext == EXT_SYM_PADJ && !blk_rows_in;
+        padj_rows = ext == EXT_SYM_PADJ && !blk_rows_in;
       }
       {
         const int nb = it + C::NS - 1;  // its slot held block it-1, consumed before (1)
@@ -595,7 +598,7 @@ __device__ __forceinline__ void ana_level_runs(const AnaStreamParams<T, L> &p, u
 // 161.4 us, cfg3 W* 101.7 / 97.1 / 96.0 us, cfg5 grad 558.9 / 555.1 / 549.2 us (with the ring blur's cap)
 #define WL_ANA_REGCAP 384
 #endif
-template <typename T, int L, bool FU, int NS, int ZV = 0, bool PLAIN = false>
+template <typename T, int L, bool FU, int NS, int ZV = 0, int KIND = 0>
 __global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? WL_ANA_REGCAP / ACfg<T, L, NS, FU>::NT : 1)
     k_ana_stream(const __grid_constant__ AnaStreamParams<T, L> p) {
   using C = ACfg<T, L, NS, FU>;
@@ -608,7 +611,7 @@ __global__ void __launch_bounds__(ACfg<T, L, NS, FU>::NT, sizeof(T) == 4 ? WL_AN
   pdl_launch_dependents();
   pdl_wait();  // the previous kernel of the stream wrote our inputs
   unsigned phase = 0;
-  ana_level_runs<T, L, FU, NS, ZV, PLAIN>(p, smem_raw, phase);
+  ana_level_runs<T, L, FU, NS, ZV, KIND>(p, smem_raw, phase);
 }
 
 // The coarse tail of a W* / W-dagger chain in one persistent launch: levels
@@ -737,10 +740,16 @@ cudaError_t launch_ana_stream_t(const AnalysisArgs &a, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   long long resident = 0;
   // the compact zero-extension instantiation (fp32, plain stores) when every block comes by TMA
-  constexpr bool HAS_PLAIN = sizeof(T) == 4;
-  const bool plain = HAS_PLAIN && p.tma && p.tma_any_block && plain_enabled();
-  auto kshort = plain ? k_ana_stream<T, L, FU, 4, ZV, HAS_PLAIN> : k_ana_stream<T, L, FU, 4, ZV, false>;
-  auto klong = plain ? k_ana_stream<T, L, FU, 0, ZV, HAS_PLAIN> : k_ana_stream<T, L, FU, 0, ZV, false>;
+  constexpr bool F32 = sizeof(T) == 4;
+  constexpr int K1 = F32 ? 1 : 0, K2 = (F32 && !FU) ? 2 : 0, K3 = (F32 && !FU) ? 3 : 0;  // instantiated kinds
+  int kind = 0;
+  if (p.tma && plain_enabled()) kind = p.tma_any_block ? K1 : (a.ext == EXT_SYM ? K2 : (a.ext == EXT_SYM_PADJ ? K3 : 0));
+  auto kshort = kind == 1 ? k_ana_stream<T, L, FU, 4, ZV, K1>
+                          : (kind == 2 ? k_ana_stream<T, L, FU, 4, ZV, K2>
+                                       : (kind == 3 ? k_ana_stream<T, L, FU, 4, ZV, K3> : k_ana_stream<T, L, FU, 4, ZV, 0>));
+  auto klong = kind == 1 ? k_ana_stream<T, L, FU, 0, ZV, K1>
+                         : (kind == 2 ? k_ana_stream<T, L, FU, 0, ZV, K2>
+                                      : (kind == 3 ? k_ana_stream<T, L, FU, 0, ZV, K3> : k_ana_stream<T, L, FU, 0, ZV, 0>));
   if (short_run) {
     e = kernel_resident(reinterpret_cast<const void *>(kshort), C4::NT, C4::smem_bytes(FU), &resident);
     if (e != cudaSuccess) return e;
