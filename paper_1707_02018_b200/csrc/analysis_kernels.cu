@@ -709,7 +709,7 @@ cudaError_t make_ana_params(const AnalysisArgs &a, AnaStreamParams<T, L> &p, boo
     p.runs = RunMap::make((long long)a.batch * p.nstrips, a.m0, resident, std::max(1, C::G * WL_ANA_MINROWS / 2), 1,
                           balanced_runs());
     const int band = p.runs.mean_rows();
-    short_run = (band + C::G - 1) / C::G <= short_run_max(3);
+    short_run = (band + C::G - 1) / C::G <= short_run_max(3, 'a');
   }
   if (short_run) {
     if (!force_short) {

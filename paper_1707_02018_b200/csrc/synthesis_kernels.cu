@@ -523,7 +523,7 @@ cudaError_t make_syn_params(const SynthesisArgs &a, SynStreamParams<T, L> &p, bo
     // one run per resident CTA when the columns allow it; even bands of >= 4 iterations
     p.runs = RunMap::make((long long)a.batch * p.nstrips, span0, resident, WL_SYN_MINROWS * C::G, 2, balanced_runs());
     const int band = p.runs.mean_rows();
-    short_run = (band / 2 + C::H - 1) / C::G + 1 <= short_run_max(2);
+    short_run = (band / 2 + C::H - 1) / C::G + 1 <= short_run_max(2, 's');
   }
   if (short_run) {
     // short runs (coarse levels): every batch of the run in flight at once

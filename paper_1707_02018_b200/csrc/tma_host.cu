@@ -127,12 +127,21 @@ bool pdl_enabled(char kind) {
   return strchr(off, kind) == nullptr;
 }
 
-int short_run_max(int dflt) {
+int short_run_max(int dflt, char kind) {
   static const int v = [] {
     const char *e = getenv("WL_SHORT_MAX");
     return e ? atoi(e) : -1;
   }();
-  return v >= 0 ? v : dflt;
+  static const int va = [] {
+    const char *e = getenv("WL_SHORT_MAX_A");  // analysis only
+    return e ? atoi(e) : -1;
+  }();
+  static const int vs = [] {
+    const char *e = getenv("WL_SHORT_MAX_S");  // synthesis only
+    return e ? atoi(e) : -1;
+  }();
+  const int k = kind == 'a' ? va : (kind == 's' ? vs : -1);
+  return k >= 0 ? k : (v >= 0 ? v : dflt);
 }
 
 cudaError_t kernel_resident(const void *kern, int nt, size_t smem, long long *resident) {

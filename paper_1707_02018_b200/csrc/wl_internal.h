@@ -171,7 +171,7 @@ cudaError_t kernel_resident(const void *kern, int nt, size_t smem, long long *re
 // Longest run (in blocks / batches) that the streaming kernels treat as short and launch with
 // every block in flight at once (4 stages): `dflt` is the kernel's measured best (analysis 3,
 // synthesis 2 on B200); WL_SHORT_MAX overrides both (0 disables; A/B switch).
-int short_run_max(int dflt);
+int short_run_max(int dflt, char kind = 0);  // kind 'a' / 's': WL_SHORT_MAX_A / WL_SHORT_MAX_S override one family
 
 // TMA loads unless WL_NO_TMA is set (debugging / A-B switch); read once per process
 bool tma_enabled();
