@@ -608,10 +608,11 @@ wl_status wl_blur_adjoint(const wl_blur_plan *bl, int64_t batch, const void *in,
 }
 
 static wl_status residual_core(const wl_blur_plan *bl, int64_t batch, const void *u, const void *b, void *s,
-                               double *f, cudaStream_t stream) {
+                               double *f, cudaStream_t stream, bool f_zeroed = false) {
   BlurArgs a;
   a.in = u; a.b = b; a.out = s; a.f = f; a.h = bl->h; a.w = bl->w;
   a.ntaps = bl->ntaps; a.taps = bl->taps; a.batch = (int)batch;
+  a.f_zeroed = f_zeroed ? 1 : 0;
   cudaError_t e = launch_blur_residual(bl->dtype, a, stream);
   if (e != cudaSuccess) return cuda_fail(e, "blur residual launch");
   return WL_OK;
@@ -623,8 +624,13 @@ namespace {
 wl_status grad_core(const wl_plan *p, const wl_blur_plan *bl, int64_t batch, const void *x, const void *b, void *g,
                     double *f_dev, char *w, const WsLayout &L, cudaStream_t s, bool true_adjoint) {
   wl_status st;
+  if (f_dev) {  // f is accumulated by the residual kernel: zeroed here, ahead of the W chain, so no memset sits
+                // between W's last level and the residual on the stream
+    cudaError_t e = launch_zero(f_dev, sizeof(double) * (size_t)batch, s);
+    if (e != cudaSuccess) return cuda_fail(e, "zero f");
+  }
   if ((st = run_synthesis(p, batch, x, w + L.u, w, L, s))) return st;          // u = W x
-  if ((st = residual_core(bl, batch, w + L.u, b, w + L.s, f_dev, s))) return st;  // s = R*(R u - b)
+  if ((st = residual_core(bl, batch, w + L.u, b, w + L.s, f_dev, s, true))) return st;  // s = R*(R u - b)
   return run_analysis(p, batch, w + L.s, g, w, L, true_adjoint, s);             // g = W* s (or W-dagger s)
 }
 }  // namespace

@@ -451,7 +451,7 @@ cudaError_t launch_ring(const BlurArgs &a, cudaStream_t s) {
   // one run per resident CTA when the columns allow it; bands of >= 2 groups
   p.runs = RunMap::make((long long)a.batch * p.nstrips, (int)a.h, resident, 2 * C::G, 1);
   const int grid = (int)std::min<long long>(p.runs.nruns(), resident);
-  if (RESID && a.f) {
+  if (RESID && a.f && !a.f_zeroed) {
     e = cudaMemsetAsync(a.f, 0, sizeof(double) * (size_t)a.batch, s);
     if (e != cudaSuccess) return e;
   }

@@ -88,6 +88,7 @@ struct BlurArgs {
   int ntaps;
   const double *taps;
   int batch;
+  int f_zeroed = 0;  // residual mode: the caller zeroed f earlier in the stream (no memset between its kernels)
 };
 
 cudaError_t launch_analysis(int dtype, const AnalysisArgs &a, cudaStream_t s);
